@@ -1,0 +1,142 @@
+/*
+ * include/ccl.h -- C ABI of the B200-native two-pass 8-connectivity connected
+ * component labeling library (libccl_b200.so), after arxiv 1606.05973
+ * ("A New Parallel Algorithm for Two-Pass Connected Component Labeling",
+ * ARemSP / PARemSP).
+ *
+ * Problem (Sec. "Proposed Algorithm"): the input is a 2-D
+ * binary image; "the connected component labeling problem is to assign a
+ * label to each object pixel so that connected object pixels have the same
+ * label", under 8-connectedness only.  The output is a 2-D array "label
+ * containing the final labels" (Alg. ARemSP / PARemSP, PAPER.md:819-820,
+ * 959-960).
+ *
+ * Output contract (bit-exact; tested against oracle/):
+ *   - pixel (r,c) is foreground  <=>  img[r*W + c] != 0          (reading A10)
+ *   - labels[r*W + c] = 0 for background, else a label in 1..N
+ *   - labels are numbered 1..N in raster (row-major) order of each component's
+ *     first pixel (BASELINE.json configs; reading A9/A13), so the
+ *     output is unique for every image
+ *   - N (flatten's k-1) is written to *n_components.
+ *
+ * Layout: row-major, pitch == W (bytes for img, int32 elements for labels).
+ * Sizes: 1 <= H, 1 <= W, (int64)H*W <= INT32_MAX.
+ *
+ * Ownership: the caller owns img, labels and n_components; the library never
+ * frees or reallocates them.  labels must not alias img.  All workspace is
+ * owned by a ccl_plan (explicit) or allocated stream-ordered from the device's
+ * default memory pool (ccl_label).
+ *
+ * Asynchrony: the device-pointer calls only enqueue work on `stream` and
+ * return; the caller synchronizes the stream before reading *n_components or
+ * labels.  Device-side faults surface at the caller's next synchronization as
+ * a CUDA error (documented, not detectable at enqueue time).
+ *
+ * Errors: arguments are validated on the host BEFORE any CUDA call, so a bad
+ * argument never launches work (and is safe to test without a GPU).
+ */
+#ifndef CCL_B200_H
+#define CCL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CCL_OK = 0,
+    CCL_INVALID_ARGUMENT = 1, /* H<1, W<1, a NULL pointer, aliasing, bad plan  */
+    CCL_TOO_LARGE = 2,        /* (int64)H*W > INT32_MAX                         */
+    CCL_CUDA_ERROR = 3,       /* a CUDA runtime call or launch failed           */
+    CCL_NCCL_ERROR = 4,       /* an NCCL call failed (sharded entry point)      */
+    CCL_OUT_OF_MEMORY = 5     /* workspace allocation failed                    */
+} ccl_status;
+
+/* Opaque stream type so this header needs no CUDA include (== cudaStream_t). */
+typedef struct CUstream_st *ccl_stream_t;
+/* Opaque NCCL communicator (== ncclComm_t). */
+typedef struct ncclComm *ccl_nccl_comm_t;
+
+/* Human-readable name of a status code; never NULL. */
+const char *ccl_status_string(ccl_status s);
+
+/* Library version as "major.minor.patch". */
+const char *ccl_version(void);
+
+/* ------------------------------------------------------------------------
+ * ccl_label -- one image on one GPU (ARemSP's contract, Alg. ARemSP
+ * PAPER.md:814-834, computed by the B200 pipeline described in DESIGN.md).
+ *   img           DEVICE pointer, H*W bytes, read only
+ *   labels        DEVICE pointer, H*W int32, written (every pixel)
+ *   n_components  DEVICE pointer to one int32, written
+ *   stream        CUDA stream (NULL = legacy default stream)
+ * Workspace is allocated and freed stream-ordered (cudaMallocAsync).
+ * ---------------------------------------------------------------------- */
+ccl_status ccl_label(const uint8_t *img, int H, int W, int32_t *labels,
+                     int32_t *n_components, ccl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Plans: preallocate the workspace for one image shape once, then label many
+ * images of that shape with no allocation.  A plan may be used by one stream
+ * at a time.
+ * ---------------------------------------------------------------------- */
+typedef struct ccl_plan_st *ccl_plan;
+
+/* Allocates device workspace for H x W images on the current device. */
+ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out);
+ccl_status ccl_plan_destroy(ccl_plan plan);
+/* Bytes of device workspace the plan holds. */
+ccl_status ccl_plan_workspace_bytes(ccl_plan plan, uint64_t *bytes);
+
+/* Same contract as ccl_label, using the plan's workspace (DEVICE pointers). */
+ccl_status ccl_plan_label(ccl_plan plan, const uint8_t *img, int32_t *labels,
+                          int32_t *n_components, ccl_stream_t stream);
+
+/* End-to-end variant with HOST buffers: copies h_img (H*W bytes) to the
+ * device, labels it, copies labels (H*W int32) and N back, and synchronizes
+ * `stream` before returning.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for full copy bandwidth.  The device
+ * staging buffers belong to the plan. */
+ccl_status ccl_plan_label_host(ccl_plan plan, const uint8_t *h_img, int32_t *h_labels,
+                               int32_t *h_n_components, ccl_stream_t stream);
+
+/* Per-kernel timing of the last ccl_plan_label call made with profiling
+ * enabled (ccl_plan_set_profiling(plan, 1)): fills up to `cap` entries of
+ * names/ms with the CUDA-event duration of each pipeline kernel, recorded on
+ * the launch stream; *count receives the number of kernels.  Synchronizes. */
+ccl_status ccl_plan_set_profiling(ccl_plan plan, int enable);
+ccl_status ccl_plan_kernel_times(ccl_plan plan, const char **names, float *ms, int cap,
+                                 int *count);
+
+/* ------------------------------------------------------------------------
+ * ccl_label_sharded -- one image split into contiguous row bands, one band
+ * per rank of an NCCL communicator (the B200 analogue of PARemSP's row
+ * chunks with per-thread label offsets).
+ * Collective: every rank of `comm` calls it with the same W and H_total.
+ *   band_img       DEVICE pointer, band_H*W bytes = global rows row0..row0+band_H-1
+ *   band_labels    DEVICE pointer, band_H*W int32: the SAME values the
+ *                  single-GPU ccl_label writes for those rows of the full image
+ *   n_components   DEVICE pointer, receives the GLOBAL N on every rank
+ * Bands are contiguous in rank order: row0 of rank k = sum of band_H of ranks
+ * < k, and sum(band_H) = H_total (checked collectively; mismatch ->
+ * CCL_INVALID_ARGUMENT on every rank).  band_H >= 1.  Synchronizes `stream`
+ * (the cross-band step needs host-visible sizes).
+ * ---------------------------------------------------------------------- */
+ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0,
+                             int H_total, int32_t *band_labels, int32_t *n_components,
+                             ccl_nccl_comm_t comm, ccl_stream_t stream);
+
+/* NCCL bootstrap helpers (torch.distributed does not expose its ncclComm_t):
+ * rank 0 creates the 128-byte unique id, the harness broadcasts it (e.g. via
+ * torch.distributed over gloo), then every rank creates its communicator on
+ * the current device. */
+ccl_status ccl_nccl_get_unique_id(uint8_t id_out[128]);
+ccl_status ccl_nccl_comm_create(const uint8_t id[128], int nranks, int rank,
+                                ccl_nccl_comm_t *comm_out);
+ccl_status ccl_nccl_comm_destroy(ccl_nccl_comm_t comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCL_B200_H */

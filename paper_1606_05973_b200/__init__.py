@@ -1,0 +1,206 @@
+"""B200-native two-pass 8-connectivity connected component labeling
+(after arxiv 1606.05973, ARemSP / PARemSP).
+
+A thin ctypes binding over the C ABI in ``include/ccl.h`` /
+``libccl_b200.so``: argument marshalling only -- every step of the labeling
+runs in the library's sm_100a kernels.  PyTorch supplies device memory and
+streams.  There is no CPU fallback: importing this package fails loudly when
+the native library is missing.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, os.environ.get("CCL_B200_LIB", "libccl_b200.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"paper_1606_05973_b200: native library {LIB_PATH} is missing; build it with "
+        "`python build_native.py product` (or __graft_entry__.build()). There is no fallback.")
+
+_L = ctypes.CDLL(LIB_PATH)
+
+CCL_OK, CCL_INVALID_ARGUMENT, CCL_TOO_LARGE, CCL_CUDA_ERROR, CCL_NCCL_ERROR, CCL_OUT_OF_MEMORY = range(6)
+
+_vp, _i, _u64p = ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)
+_L.ccl_status_string.argtypes = [_i]
+_L.ccl_status_string.restype = ctypes.c_char_p
+_L.ccl_version.argtypes = []
+_L.ccl_version.restype = ctypes.c_char_p
+_L.ccl_label.argtypes = [_vp, _i, _i, _vp, _vp, _vp]
+_L.ccl_label.restype = _i
+_L.ccl_plan_create.argtypes = [_i, _i, ctypes.POINTER(_vp)]
+_L.ccl_plan_create.restype = _i
+_L.ccl_plan_destroy.argtypes = [_vp]
+_L.ccl_plan_destroy.restype = _i
+_L.ccl_plan_workspace_bytes.argtypes = [_vp, _u64p]
+_L.ccl_plan_workspace_bytes.restype = _i
+_L.ccl_plan_label.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_L.ccl_plan_label.restype = _i
+_L.ccl_plan_label_host.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_L.ccl_plan_label_host.restype = _i
+_L.ccl_plan_set_profiling.argtypes = [_vp, _i]
+_L.ccl_plan_set_profiling.restype = _i
+_L.ccl_plan_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p),
+                                     ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(_i)]
+_L.ccl_plan_kernel_times.restype = _i
+_L.ccl_label_sharded.argtypes = [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]
+_L.ccl_label_sharded.restype = _i
+_L.ccl_nccl_get_unique_id.argtypes = [_vp]
+_L.ccl_nccl_get_unique_id.restype = _i
+_L.ccl_nccl_comm_create.argtypes = [_vp, _i, _i, ctypes.POINTER(_vp)]
+_L.ccl_nccl_comm_create.restype = _i
+_L.ccl_nccl_comm_destroy.argtypes = [_vp]
+_L.ccl_nccl_comm_destroy.restype = _i
+
+
+class CCLError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)}")
+
+
+def status_string(status):
+    return _L.ccl_status_string(int(status)).decode()
+
+
+def version():
+    return _L.ccl_version().decode()
+
+
+def _check(rc, what):
+    if rc != CCL_OK:
+        raise CCLError(rc, what)
+
+
+def _stream_handle(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_img(img):
+    if not isinstance(img, torch.Tensor) or img.dtype != torch.uint8 or img.dim() != 2:
+        raise TypeError("img must be a 2-D torch.uint8 tensor")
+    if not img.is_cuda:
+        raise TypeError("img must be a CUDA tensor (use Plan.label_host for host buffers)")
+    if not img.is_contiguous():
+        raise ValueError("img must be contiguous (pitch == W)")
+
+
+def label(img, out=None, n_out=None, stream=None):
+    """Labels a 2-D uint8 CUDA image (foreground <=> != 0) with 8-connectivity.
+    Returns (labels int32 HxW on the same device, n_components int32 tensor [1]).
+    Labels are 1..N in raster order of each component's first pixel, 0 = background.
+    Asynchronous on `stream` (default: current stream)."""
+    _check_img(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.int32, device=img.device)
+    if n_out is None:
+        n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+    _check(_L.ccl_label(img.data_ptr(), H, W, out.data_ptr(), n_out.data_ptr(),
+                        _stream_handle(stream)), "ccl_label")
+    return out, n_out
+
+
+class Plan:
+    """Preallocated workspace for one image shape (ccl_plan_* in include/ccl.h)."""
+
+    def __init__(self, H, W, device=None):
+        self.H, self.W = int(H), int(W)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._p = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(_L.ccl_plan_create(self.H, self.W, ctypes.byref(self._p)), "ccl_plan_create")
+
+    def workspace_bytes(self):
+        b = ctypes.c_uint64()
+        _check(_L.ccl_plan_workspace_bytes(self._p, ctypes.byref(b)), "ccl_plan_workspace_bytes")
+        return b.value
+
+    def label(self, img, out=None, n_out=None, stream=None):
+        _check_img(img)
+        if tuple(img.shape) != (self.H, self.W):
+            raise ValueError(f"plan is for {self.H}x{self.W}, got {tuple(img.shape)}")
+        if out is None:
+            out = torch.empty((self.H, self.W), dtype=torch.int32, device=img.device)
+        if n_out is None:
+            n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+        _check(_L.ccl_plan_label(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
+                                 _stream_handle(stream)), "ccl_plan_label")
+        return out, n_out
+
+    def label_host(self, img, out, n_out, stream=None):
+        """End to end with HOST (ideally pinned) tensors: H2D copy, label, D2H
+        copy, stream synchronize -- all inside the library."""
+        for t, dt in ((img, torch.uint8), (out, torch.int32), (n_out, torch.int32)):
+            if t.is_cuda or t.dtype != dt or not t.is_contiguous():
+                raise TypeError("label_host takes contiguous host tensors (uint8 img, int32 out/n)")
+        _check(_L.ccl_plan_label_host(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
+                                      _stream_handle(stream)), "ccl_plan_label_host")
+        return out, n_out
+
+    def set_profiling(self, enable=True):
+        _check(_L.ccl_plan_set_profiling(self._p, int(bool(enable))), "ccl_plan_set_profiling")
+
+    def kernel_times(self):
+        """{kernel name: ms} of the last profiled label() call (CUDA events on its stream)."""
+        cap = 16
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int()
+        _check(_L.ccl_plan_kernel_times(self._p, names, ms, cap, ctypes.byref(n)), "ccl_plan_kernel_times")
+        return {names[i].decode(): float(ms[i]) for i in range(n.value)}
+
+    def close(self):
+        if self._p:
+            _L.ccl_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ multi-GPU
+def nccl_unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_L.ccl_nccl_get_unique_id(buf), "ccl_nccl_get_unique_id")
+    return bytes(buf)
+
+
+class NcclComm:
+    """NCCL communicator for ccl_label_sharded (torch does not expose its own)."""
+
+    def __init__(self, uid, nranks, rank):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._c = ctypes.c_void_p()
+        _check(_L.ccl_nccl_comm_create(buf, nranks, rank, ctypes.byref(self._c)), "ccl_nccl_comm_create")
+
+    @property
+    def handle(self):
+        return self._c
+
+    def close(self):
+        if self._c:
+            _L.ccl_nccl_comm_destroy(self._c)
+            self._c = ctypes.c_void_p()
+
+
+def label_sharded(band_img, row0, H_total, comm, out=None, n_out=None, stream=None):
+    """Collective: this rank's band of global rows row0..row0+band_H-1.  Labels
+    and N are global (equal to the single-GPU result for these rows)."""
+    _check_img(band_img)
+    bh, W = band_img.shape
+    if out is None:
+        out = torch.empty((bh, W), dtype=torch.int32, device=band_img.device)
+    if n_out is None:
+        n_out = torch.empty(1, dtype=torch.int32, device=band_img.device)
+    _check(_L.ccl_label_sharded(band_img.data_ptr(), bh, W, int(row0), int(H_total), out.data_ptr(),
+                                n_out.data_ptr(), comm.handle, _stream_handle(stream)),
+           "ccl_label_sharded")
+    return out, n_out

@@ -1,0 +1,267 @@
+// ccl_api.cu -- the extern "C" boundary of libccl_b200.so (include/ccl.h).
+// Argument checks run on the host before any CUDA call.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <new>
+
+#include "ccl.h"
+#include "ccl_internal.cuh"
+
+namespace cclb {
+
+Geometry make_geometry(int H, int W) {
+    Geometry g;
+    g.H = H;
+    g.W = W;
+    g.WW = (W + 31) / 32;
+    g.nTx = (W + TW - 1) / TW;
+    g.nTy = (H + TH - 1) / TH;
+    g.nT = g.nTx * g.nTy;
+    g.nseg = H * g.nTx;
+    g.nscan = (g.nseg + SCAN_TILE - 1) / SCAN_TILE;
+    g.aligned = (W % 16) == 0;
+    return g;
+}
+
+enum {
+    A_BM, A_RUNLAB, A_LMAP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_GPARENT, A_GKEY, A_GNODESEG,
+    A_GNODERANK, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE,
+    A_TICKET, A_COUNT
+};
+
+void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
+    const size_t nT = (size_t)g.nT, H = (size_t)g.H;
+    const size_t sz[A_COUNT] = {
+        H * g.WW * 4,                   // bm
+        H * g.nTx * MAXRUN * 2,         // runlab
+        nT * CAP * 2,                   // lmap
+        nT * CAPC * 4,                  // compkey
+        nT * CAPC * 4,                  // compnode
+        nT * CAPC * 4,                  // comprank
+        nT * CAPB * 4,                  // gparent
+        nT * CAPB * 4,                  // gkey
+        nT * CAPB * 4,                  // gnodeseg
+        nT * CAPB * 4,                  // gnoderank
+        nT * MAXRUN * 4,                // topnode
+        nT * MAXRUN * 4,                // botnode
+        (size_t)g.nTx * H * 4,          // leftnode
+        (size_t)g.nTx * H * 4,          // rightnode
+        nT * META * 4,                  // meta
+        (size_t)g.nseg * 4,             // segcnt
+        (size_t)g.nseg * 4,             // segoff
+        (size_t)g.nscan * 8,            // scanstate
+        16,                             // ticket
+    };
+    size_t o = 0;
+    for (int i = 0; i < A_COUNT; i++) {
+        offs[i] = o;
+        o += (sz[i] + 255) & ~(size_t)255;
+    }
+    *total = o;
+}
+
+Workspace workspace_bind(const Geometry &g, void *base) {
+    size_t offs[A_COUNT], total;
+    workspace_layout(g, offs, &total);
+    char *b = static_cast<char *>(base);
+    Workspace w;
+    w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
+    w.runlab = reinterpret_cast<uint16_t *>(b + offs[A_RUNLAB]);
+    w.lmap = reinterpret_cast<uint16_t *>(b + offs[A_LMAP]);
+    w.compkey = reinterpret_cast<int32_t *>(b + offs[A_COMPKEY]);
+    w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);
+    w.comprank = reinterpret_cast<uint32_t *>(b + offs[A_COMPRANK]);
+    w.gparent = reinterpret_cast<int32_t *>(b + offs[A_GPARENT]);
+    w.gkey = reinterpret_cast<int32_t *>(b + offs[A_GKEY]);
+    w.gnodeseg = reinterpret_cast<int32_t *>(b + offs[A_GNODESEG]);
+    w.gnoderank = reinterpret_cast<int32_t *>(b + offs[A_GNODERANK]);
+    w.topnode = reinterpret_cast<int32_t *>(b + offs[A_TOP]);
+    w.botnode = reinterpret_cast<int32_t *>(b + offs[A_BOT]);
+    w.leftnode = reinterpret_cast<int32_t *>(b + offs[A_LEFT]);
+    w.rightnode = reinterpret_cast<int32_t *>(b + offs[A_RIGHT]);
+    w.meta = reinterpret_cast<int32_t *>(b + offs[A_META]);
+    w.segcnt = reinterpret_cast<int32_t *>(b + offs[A_SEGCNT]);
+    w.segoff = reinterpret_cast<int32_t *>(b + offs[A_SEGOFF]);
+    w.scanstate = reinterpret_cast<unsigned long long *>(b + offs[A_SCANSTATE]);
+    w.ticket = reinterpret_cast<int32_t *>(b + offs[A_TICKET]);
+    return w;
+}
+
+}  // namespace cclb
+
+using namespace cclb;
+
+struct ccl_plan_st {
+    Geometry g;
+    void *ws_mem = nullptr;
+    size_t ws_bytes = 0;
+    Workspace ws;
+    uint8_t *d_img = nullptr;   // staging buffers for ccl_plan_label_host
+    int32_t *d_lab = nullptr;
+    int32_t *d_n = nullptr;
+    bool profiling = false;
+    cudaEvent_t ev[K_COUNT + 1] = {};
+    bool have_times = false;
+};
+
+static ccl_status check_shape(int H, int W) {
+    if (H < 1 || W < 1) return CCL_INVALID_ARGUMENT;
+    if ((int64_t)H * (int64_t)W > (int64_t)INT32_MAX) return CCL_TOO_LARGE;
+    return CCL_OK;
+}
+
+static ccl_status check_buffers(const void *img, const void *labels, const void *n, int H, int W) {
+    if (!img || !labels || !n) return CCL_INVALID_ARGUMENT;
+    const char *a = static_cast<const char *>(img);
+    const char *l = static_cast<const char *>(labels);
+    const size_t nb = (size_t)H * (size_t)W;
+    if (a < l + nb * 4 && l < a + nb) return CCL_INVALID_ARGUMENT;  // labels alias img
+    return CCL_OK;
+}
+
+extern "C" {
+
+const char *ccl_status_string(ccl_status s) {
+    switch (s) {
+        case CCL_OK: return "CCL_OK";
+        case CCL_INVALID_ARGUMENT: return "CCL_INVALID_ARGUMENT";
+        case CCL_TOO_LARGE: return "CCL_TOO_LARGE";
+        case CCL_CUDA_ERROR: return "CCL_CUDA_ERROR";
+        case CCL_NCCL_ERROR: return "CCL_NCCL_ERROR";
+        case CCL_OUT_OF_MEMORY: return "CCL_OUT_OF_MEMORY";
+    }
+    return "CCL_UNKNOWN_STATUS";
+}
+
+const char *ccl_version(void) { return "0.1.0"; }
+
+ccl_status ccl_label(const uint8_t *img, int H, int W, int32_t *labels, int32_t *n_components,
+                     ccl_stream_t stream) {
+    ccl_status st = check_shape(H, W);
+    if (st != CCL_OK) return st;
+    if ((st = check_buffers(img, labels, n_components, H, W)) != CCL_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Geometry g = make_geometry(H, W);
+    size_t offs[32], total;
+    workspace_layout(g, offs, &total);
+    void *mem = nullptr;
+    cudaError_t e = cudaMallocAsync(&mem, total, s);
+    if (e == cudaErrorMemoryAllocation) return CCL_OUT_OF_MEMORY;
+    if (e != cudaSuccess) return CCL_CUDA_ERROR;
+    Workspace ws = workspace_bind(g, mem);
+    e = run_pipeline(g, ws, img, labels, n_components, s, nullptr);
+    cudaError_t e2 = cudaFreeAsync(mem, s);
+    if (e != cudaSuccess || e2 != cudaSuccess) return CCL_CUDA_ERROR;
+    return CCL_OK;
+}
+
+ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out) {
+    if (!plan_out) return CCL_INVALID_ARGUMENT;
+    *plan_out = nullptr;
+    ccl_status st = check_shape(H, W);
+    if (st != CCL_OK) return st;
+    ccl_plan p = new (std::nothrow) ccl_plan_st;
+    if (!p) return CCL_OUT_OF_MEMORY;
+    p->g = make_geometry(H, W);
+    size_t offs[32];
+    workspace_layout(p->g, offs, &p->ws_bytes);
+    cudaError_t e = cudaMalloc(&p->ws_mem, p->ws_bytes);
+    if (e != cudaSuccess) {
+        delete p;
+        return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
+    }
+    p->ws = workspace_bind(p->g, p->ws_mem);
+    *plan_out = p;
+    return CCL_OK;
+}
+
+ccl_status ccl_plan_destroy(ccl_plan p) {
+    if (!p) return CCL_INVALID_ARGUMENT;
+    cudaError_t e = cudaSuccess;
+    if (p->ws_mem) e = cudaFree(p->ws_mem);
+    if (p->d_img) cudaFree(p->d_img);
+    if (p->d_lab) cudaFree(p->d_lab);
+    if (p->d_n) cudaFree(p->d_n);
+    for (auto &ev : p->ev)
+        if (ev) cudaEventDestroy(ev);
+    delete p;
+    return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+}
+
+ccl_status ccl_plan_workspace_bytes(ccl_plan p, uint64_t *bytes) {
+    if (!p || !bytes) return CCL_INVALID_ARGUMENT;
+    *bytes = p->ws_bytes;
+    return CCL_OK;
+}
+
+ccl_status ccl_plan_label(ccl_plan p, const uint8_t *img, int32_t *labels, int32_t *n_components,
+                          ccl_stream_t stream) {
+    if (!p) return CCL_INVALID_ARGUMENT;
+    ccl_status st = check_buffers(img, labels, n_components, p->g.H, p->g.W);
+    if (st != CCL_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (p->profiling && !p->ev[0]) {
+        for (auto &ev : p->ev)
+            if (cudaEventCreate(&ev) != cudaSuccess) return CCL_CUDA_ERROR;
+    }
+    cudaError_t e = run_pipeline(p->g, p->ws, img, labels, n_components, s,
+                                 p->profiling ? p->ev : nullptr);
+    p->have_times = p->profiling;
+    return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+}
+
+ccl_status ccl_plan_label_host(ccl_plan p, const uint8_t *h_img, int32_t *h_labels,
+                               int32_t *h_n_components, ccl_stream_t stream) {
+    if (!p || !h_img || !h_labels || !h_n_components) return CCL_INVALID_ARGUMENT;
+    const size_t n = (size_t)p->g.H * (size_t)p->g.W;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (!p->d_img) {
+        if ((e = cudaMalloc(&p->d_img, n)) != cudaSuccess ||
+            (e = cudaMalloc(&p->d_lab, n * 4)) != cudaSuccess ||
+            (e = cudaMalloc(&p->d_n, 16)) != cudaSuccess)
+            return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
+    }
+    if (cudaMemcpyAsync(p->d_img, h_img, n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return CCL_CUDA_ERROR;
+    ccl_status st = ccl_plan_label(p, p->d_img, p->d_lab, p->d_n, stream);
+    if (st != CCL_OK) return st;
+    if (cudaMemcpyAsync(h_labels, p->d_lab, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(h_n_components, p->d_n, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return CCL_CUDA_ERROR;
+    return cudaStreamSynchronize(s) == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+}
+
+ccl_status ccl_plan_set_profiling(ccl_plan p, int enable) {
+    if (!p) return CCL_INVALID_ARGUMENT;
+    p->profiling = enable != 0;
+    return CCL_OK;
+}
+
+ccl_status ccl_plan_kernel_times(ccl_plan p, const char **names, float *ms, int cap, int *count) {
+    if (!p || !count) return CCL_INVALID_ARGUMENT;
+    *count = K_COUNT;
+    if (!p->have_times) return CCL_INVALID_ARGUMENT;
+    if (cudaEventSynchronize(p->ev[K_COUNT]) != cudaSuccess) return CCL_CUDA_ERROR;
+    for (int i = 0; i < K_COUNT && i < cap; i++) {
+        if (names) names[i] = kKernelNames[i];
+        if (ms && cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess)
+            return CCL_CUDA_ERROR;
+    }
+    return CCL_OK;
+}
+
+}  // extern "C"
+
+// Development hook (not part of include/ccl.h): base pointer and byte offsets
+// of the plan's workspace arrays, in Workspace declaration order.
+extern "C" int ccl_debug_workspace(ccl_plan p, void **base, uint64_t *offs, int cap) {
+    if (!p || !base || !offs) return CCL_INVALID_ARGUMENT;
+    size_t o[32], total;
+    workspace_layout(p->g, o, &total);
+    *base = p->ws_mem;
+    for (int i = 0; i < A_COUNT && i < cap; i++) offs[i] = o[i];
+    return A_COUNT;
+}

@@ -1,0 +1,77 @@
+// ccl_internal.cuh -- shared definitions of the B200 CCL pipeline (product
+// path).  No code here is shared with oracle/ (DESIGN.md "Independence").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cclb {
+
+// ---- tiling ------------------------------------
+constexpr int TW = 1024;               // tile width in pixels: one warp-row, 32 lanes x 32 bits
+constexpr int WPR = TW / 32;           // 32-bit words per tile row
+constexpr int NW = 8;                  // warps per CTA (K1, K5)
+constexpr int S = 4;                   // rows per strip; warp w scans rows [w*S, w*S+S) in order
+constexpr int TH = NW * S;             // tile height (32)
+constexpr int MAXRUN = TW / 2;         // max runs in one tile row
+// New provisional labels are created only at run heads with no foreground in
+// the row above (within the strip); such heads are pairwise non-adjacent in
+// the king's graph, so a strip creates at most ceil(S/2)*ceil(TW/2) labels.
+constexpr int CAPS = ((S + 1) / 2) * (TW / 2);
+constexpr int CAP = NW * CAPS;         // provisional labels per tile (8192 < 65536: u16)
+constexpr int CAPC = CAP;              // tile-local components per tile
+constexpr int CAPB = 2 * MAXRUN + TH;  // components touching the tile border
+constexpr int META = 16;               // ints of per-tile metadata
+constexpr int META_NCOMP = 0, META_NBORDER = 1, META_ROWS = 2, META_USED = 4;  // USED..USED+NW
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+struct Geometry {
+    int H, W;
+    int WW;        // 32-bit words per image row = ceil(W/32)
+    int nTx, nTy;  // tile grid
+    int nT;        // nTx * nTy
+    int nseg;      // H * nTx: (row, tile-column) segments in raster order
+    int nscan;     // decoupled-lookback partitions over the segments
+    int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
+};
+
+// Device workspace (all arrays carved from one allocation; see ccl_api.cu).
+struct Workspace {
+    uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
+    uint16_t *runlab;     // [H][nTx][MAXRUN]  provisional label of each run of each tile row
+    uint16_t *lmap;       // [nT][CAP]         provisional label -> tile-local component
+    int32_t *compkey;     // [nT][CAPC]        raster index of the component's first pixel
+    int32_t *compnode;    // [nT][CAPC]        border-node id, or -1 (component inside the tile)
+    uint32_t *comprank;   // [nT][CAPC]        (row<<16 | rank within its segment) for global roots
+    int32_t *gparent;     // [nT][CAPB]        global union-find over border components
+    int32_t *gkey;        // [nT][CAPB]        raster key of the node's first pixel
+    int32_t *gnodeseg;    // [nT][CAPB]        segment of a root node's first pixel
+    int32_t *gnoderank;   // [nT][CAPB]        rank of a root node inside that segment
+    int32_t *topnode;     // [nT][MAXRUN]      node of each run of the tile's first row
+    int32_t *botnode;     // [nT][MAXRUN]      node of each run of the tile's last row
+    int32_t *leftnode;    // [nTx][H]          node of the pixel in the tile's first column
+    int32_t *rightnode;   // [nTx][H]          node of the pixel in the tile's last column
+    int32_t *meta;        // [nT][META]
+    int32_t *segcnt;      // [nseg]            global roots whose first pixel lies in the segment
+    int32_t *segoff;      // [nseg]            exclusive prefix of segcnt (raster order)
+    unsigned long long *scanstate;  // [nscan] decoupled-lookback descriptors
+    int32_t *ticket;      // [1]               dynamic partition counter
+};
+
+Geometry make_geometry(int H, int W);
+// Offsets of every Workspace array inside one allocation of *total bytes.
+void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
+Workspace workspace_bind(const Geometry &g, void *base);
+
+enum { K_TILE = 0, K_BORDER, K_ROOTS, K_SCAN, K_WRITE, K_COUNT };
+extern const char *const kKernelNames[K_COUNT];
+
+// Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it
+// must hold K_COUNT+1 events; event i is recorded before kernel i.
+cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
+                         int32_t *labels, int32_t *n_components, cudaStream_t stream,
+                         cudaEvent_t *ev);
+
+}  // namespace cclb

@@ -1,0 +1,151 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle:
+bit-exact labels and N on the same seeded inputs (integer work: zero
+tolerance).  Sizes span several 32x1024 tiles with ragged tails; the full
+BASELINE configs are compared whole (the oracle labels 466 Mpx in seconds)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import pins
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ccl = pytest.importorskip("paper_1606_05973_b200") if torch.cuda.is_available() else None
+
+
+def gpu_label(img, plan=None):
+    t = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    if plan is None:
+        lab, n = ccl.label(t)
+    else:
+        lab, n = plan.label(t)
+    torch.cuda.synchronize()
+    return lab.cpu().numpy(), int(n.item())
+
+
+def assert_same(img, tag=""):
+    lg, ng = gpu_label(img)
+    lo, no = oracle.label(img)
+    if ng != no or not np.array_equal(lg, lo):
+        bad = np.argwhere(lg != lo)
+        first = tuple(bad[0]) if len(bad) else None
+        raise AssertionError(f"{tag} {img.shape}: N gpu={ng} oracle={no}; {len(bad)} pixels differ, first at {first}")
+
+
+SHAPES = [(1, 1), (1, 2), (2, 1), (1, 1000), (1, 1025), (3, 7), (7, 3), (31, 1023), (32, 1024),
+          (33, 1025), (64, 2048), (65, 2049), (95, 3001), (100, 1040), (257, 4097),
+          (40, 17), (17, 40), (500, 96), (64, 31), (1, 4096), (4096, 1), (300, 2052)]
+
+
+@pytest.mark.parametrize("H,W", SHAPES)
+@pytest.mark.parametrize("p", [0.1, 0.41, 0.5, 0.7, 0.95])
+def test_random_shapes(H, W, p):
+    img = synth.bernoulli(H, W, p, seed=H * 7919 + W)
+    assert_same(img, f"bernoulli p={p}")
+
+
+@pytest.mark.parametrize("name", ["c1_bernoulli_512", "c2_blobs_1024", "c3_percolation_8192",
+                                  "c4_voronoi_21600", "c5a_serpentine_16384"])
+def test_recipes_at_moderate_size(name):
+    for (H, W) in [(777, 3333), (1000, 1000), (64, 5000)]:
+        assert_same(synth.scaled(name, H, W), name)
+
+
+def test_structured_edge_cases():
+    for (H, W) in [(2, 2), (5, 5), (33, 1030), (100, 2100), (97, 1024)]:
+        assert_same(np.zeros((H, W), np.uint8), "zeros")
+        assert_same(np.ones((H, W), np.uint8), "ones")
+        assert_same(synth.serpentine(H, W), "serpentine")
+        assert_same(synth.comb(H, W), "comb")
+        img = np.zeros((H, W), np.uint8); img[::2, ::2] = 1
+        assert_same(img, "lattice")
+        img = ((np.add.outer(np.arange(H), np.arange(W)) % 2) == 0).astype(np.uint8)
+        assert_same(img, "checkerboard")
+        img = np.zeros((H, W), np.uint8); img[:, ::2] = 1
+        assert_same(img, "vstripes")
+        img = np.zeros((H, W), np.uint8); img[::2, :] = 1
+        assert_same(img, "hstripes")
+
+
+def test_nonbinary_bytes():
+    rng = np.random.default_rng(9)
+    img = (rng.integers(1, 256, size=(300, 2100)) * (rng.random((300, 2100)) < 0.45)).astype(np.uint8)
+    assert_same(img, "bytes")
+
+
+def _mosaic(h, w, gap, off_r, off_c, cols):
+    """Every h x w binary pattern once, separated by `gap` background pixels and
+    shifted by (off_r, off_c) so patterns straddle tile edges."""
+    n = 1 << (h * w)
+    rows = (n + cols - 1) // cols
+    H = off_r + rows * (h + gap)
+    W = off_c + cols * (w + gap)
+    img = np.zeros((H, W), np.uint8)
+    m = np.arange(n)
+    bits = ((m[:, None] >> np.arange(h * w)[None, :]) & 1).astype(np.uint8).reshape(n, h, w)
+    for k in range(n):
+        r, c = divmod(k, cols)
+        img[off_r + r * (h + gap): off_r + r * (h + gap) + h, off_c + c * (w + gap): off_c + c * (w + gap) + w] = bits[k]
+    return img
+
+
+@pytest.mark.parametrize("off", [(0, 0), (30, 1020), (31, 1022), (1, 1)])
+def test_exhaustive_4x4_mosaic(off):
+    """All 65,536 4x4 patterns, packed so many straddle tile
+    boundaries (tile = 32 x 1024)."""
+    img = _mosaic(4, 4, 1, off[0], off[1], cols=410)
+    assert_same(img, f"mosaic{off}")
+
+
+def test_exhaustive_3x5_mosaic_no_gap():
+    """Patterns touching each other (gap 0) create long random structures."""
+    img = _mosaic(3, 5, 0, 7, 1019, cols=205)
+    assert_same(img, "mosaic-nogap")
+
+
+def test_determinism_and_plan_reuse():
+    img = synth.scaled("c3_percolation_8192", 1500, 4100)
+    plan = ccl.Plan(1500, 4100)
+    ref = gpu_label(img, plan)
+    for _ in range(20):
+        lab, n = gpu_label(img, plan)
+        assert n == ref[1] and np.array_equal(lab, ref[0])
+    lo, no = oracle.label(img)
+    assert no == ref[1] and np.array_equal(lo, ref[0])
+
+
+def test_label_host_end_to_end():
+    img = synth.scaled("c4_voronoi_21600", 2000, 3000)
+    plan = ccl.Plan(2000, 3000)
+    h_img = torch.from_numpy(img).pin_memory()
+    h_lab = torch.empty((2000, 3000), dtype=torch.int32).pin_memory()
+    h_n = torch.empty(1, dtype=torch.int32).pin_memory()
+    plan.label_host(h_img, h_lab, h_n)
+    lo, no = oracle.label(img)
+    assert int(h_n[0]) == no and np.array_equal(h_lab.numpy(), lo)
+
+
+def test_kernel_times_profiling():
+    img = torch.from_numpy(synth.bernoulli(640, 2048, 0.5, 3)).cuda()
+    plan = ccl.Plan(640, 2048)
+    plan.set_profiling(True)
+    plan.label(img)
+    t = plan.kernel_times()
+    assert set(t) == {"k_tile_local", "k_border", "k_roots", "k_scan", "k_write"}
+    assert all(v >= 0 for v in t.values())
+
+
+@pytest.mark.parametrize("name", list(synth.CONFIGS))
+def test_full_configs_bit_exact(name):
+    """Every BASELINE config at full size, whole-image bit-exact, in the
+    launch configuration bench.py times (a plan, default stream)."""
+    img = synth.generate(name)
+    H, W = img.shape
+    plan = ccl.Plan(H, W)
+    lg, ng = gpu_label(img, plan)
+    lo, no = oracle.label(img)
+    assert ng == no, (name, ng, no)
+    assert np.array_equal(lg, lo), name
+    del plan
