@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 CCL hot path (BASELINE.json metric:
+"8-conn CCL Gpixel/s on 21600^2 image at 1/2/4/8 B200; % of HBM roofline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the whole hot path (all SURVEY.md section 8(a) rows:
+load+predicate, tile-local scan+union, border merge, flatten/root ranking,
+decoupled-lookback numbering, label write) over the 21600x21600 C4 workload
+(configs[3]: 20,000-cell Voronoi class map + 5% flips), input resident in HBM.
+At N>1 (torchrun) the image is split into row bands, one per rank
+(ccl_label_sharded, NCCL over NVLink); value = H*W / max-over-ranks step time.
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "8-conn CCL Gpixel/s on 21600² image at 1/2/4/8 B200; % of HBM roofline"
+WORKLOAD = "c4_voronoi_21600"
+# algorithmic bytes per pixel: 1 B image read + 4 B label write
+ALG_BYTES_PER_PX = {"path": 5, "k_tile_local": 1, "k_write": 4,
+                    "k_border": 0, "k_roots": 0, "k_scan": 0}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=WORKLOAD)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-runs", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    return ap.parse_args()
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: STREAM-style copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s earlier measurement on this pool)"
+
+
+def ncu_traffic(kernel, workload):
+    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[workload][kernel]
+        return float(e["dram_bytes_read"]) + float(e["dram_bytes_write"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clocks and clock-event reasons through NVML in a thread while
+    the timed region runs (the recipe's nvidia-smi clocks line, via the same
+    library)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x100: "display_clock_setting",
+               0x10: "sync_boost", 0x1: "gpu_idle"}
+
+    def __init__(self, device_index, period_s=0.002):
+        self.samples, self.reasons = [], 0
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device_index]) if vis else device_index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        n = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM))
+                self.reasons |= n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def report(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        reasons = [v for k, v in sorted(self.REASONS.items()) if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def time_oracle(img, runs):
+    import oracle
+    ts, out = [], None
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        out = oracle.label(img)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), out
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """The reference arm for this tier: the CPU oracle as it stands (plain C
+    ARemSP + canonical renumbering, single-threaded) on the same workload."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import synth
+    img = synth.generate(args.workload)
+    H, W = img.shape
+    import oracle
+    for _ in range(args.warmup):
+        oracle.label(img)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.label(img)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    v = H * W / t / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Gpx/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": args.workload, "H": H, "W": W},
+        "cpu_baseline": {"value": v, "unit": "Gpx/s", "cores": 1, "kind": "oracle",
+                         "sample": f"full {H}x{W} {args.workload} image per step (single-threaded C oracle)"},
+        "e2e": {"value": v, "unit": "Gpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import synth
+    import paper_1606_05973_b200 as ccl
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    img = synth.generate(args.workload)
+    H, W = img.shape
+    # contiguous row bands, remainder to the last ranks (PARemSP chunking)
+    bands = [H // ws + (1 if k >= ws - H % ws else 0) for k in range(ws)]
+    row0 = sum(bands[:rank])
+    bh = bands[rank]
+    band = np.ascontiguousarray(img[row0:row0 + bh])
+    d_img = torch.from_numpy(band).to(dev)
+    out = torch.empty((bh, W), dtype=torch.int32, device=dev)
+    n_out = torch.empty(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    if ws == 1:
+        plan = ccl.Plan(H, W, device=dev)
+        step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
+        nT = ((W + 1023) // 1024) * ((H + 31) // 32)
+        launches_per_step = 5 if nT > 1 else 4
+    else:
+        uid = ccl.nccl_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = ccl.NcclComm(obj[0], ws, rank)
+        step = lambda: ccl.label_sharded(d_img, row0, H, comm, out, n_out)  # noqa: E731
+        plan = None
+        launches_per_step = None
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    if plan is not None:
+        plan.set_profiling(args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = H * W / (ms * 1e-3) / 1e9
+    result_labels = out.cpu().numpy() if not args.no_parity else None
+    n_gpu = int(n_out.item())
+
+    peak, peak_src = peak_hbm()
+    roofline = None
+    ktimes = None
+    if plan is not None:
+        ktimes = plan.kernel_times()
+        plan.set_profiling(0)
+        dom = max(("k_tile_local", "k_write"), key=lambda k: ktimes[k])
+        alg = ALG_BYTES_PER_PX[dom] * H * W
+        ach = alg / (ktimes[dom] * 1e-3) / 1e9
+        traffic = ncu_traffic(dom, args.workload)
+        path_ach = ALG_BYTES_PER_PX["path"] * H * W / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+                    "kernel_ms": ktimes,
+                    "path": {"achieved": path_ach, "frac": path_ach / peak,
+                             "algorithmic_bytes_per_step": ALG_BYTES_PER_PX["path"] * H * W}}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gpx/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": args.workload, "H": H, "W": W, "bands": bands,
+                   "l2": "inputs larger than L2 (466.6 MB image in, 1.87 GB labels out vs 126 MB L2); no flush"},
+        "clocks": clk.report(),
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+        "roofline": roofline,
+    }
+
+    # ---- end to end through the public API with host buffers (N=1)
+    if ws == 1 and not args.no_e2e:
+        h_img = torch.from_numpy(img).pin_memory()
+        h_lab = torch.empty((H, W), dtype=torch.int32).pin_memory()
+        h_n = torch.empty(1, dtype=torch.int32).pin_memory()
+        plan.label_host(h_img, h_lab, h_n)  # warm the staging buffers
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.label_host(h_img, h_lab, h_n)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a.elapsed_time(b) / args.e2e_steps
+        line["e2e"] = {"value": H * W / (ems * 1e-3) / 1e9, "unit": "Gpx/s",
+                       "h2d_bytes_per_step": H * W, "d2h_bytes_per_step": H * W * 4 + 4,
+                       "ms_per_step": ems}
+
+    # ---- CPU baseline (the oracle as it stands) + parity of the timed output
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        t, (lab_o, n_o) = time_oracle(img, args.cpu_runs)
+        line["cpu_baseline"] = {"value": H * W / t / 1e9, "unit": "Gpx/s", "cores": 1, "kind": "oracle",
+                                "sample": f"full {H}x{W} {args.workload} image, median of {args.cpu_runs} runs, "
+                                          "single-threaded C oracle (ARemSP + canonical renumbering)"}
+        if result_labels is not None:
+            same = (n_o == n_gpu) and bool(np.array_equal(lab_o, result_labels))
+            line["parity"] = {"vs": "oracle", "bit_exact": same, "n_components": n_gpu}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

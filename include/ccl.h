@@ -101,11 +101,14 @@ ccl_status ccl_plan_label(ccl_plan plan, const uint8_t *img, int32_t *labels,
 ccl_status ccl_plan_label_host(ccl_plan plan, const uint8_t *h_img, int32_t *h_labels,
                                int32_t *h_n_components, ccl_stream_t stream);
 
-/* Per-kernel timing of the last ccl_plan_label call made with profiling
- * enabled (ccl_plan_set_profiling(plan, 1)): fills up to `cap` entries of
- * names/ms with the CUDA-event duration of each pipeline kernel, recorded on
- * the launch stream; *count receives the number of kernels.  Synchronizes. */
-ccl_status ccl_plan_set_profiling(ccl_plan plan, int enable);
+/* Per-kernel timing.  ccl_plan_set_profiling(plan, n) arms a ring of n sets
+ * of CUDA events (n = 0 disarms): every later ccl_plan_label call records one
+ * event before each pipeline kernel and one after the last, on the launch
+ * stream (no synchronization).  ccl_plan_kernel_times fills up to `cap`
+ * entries of names/ms with each kernel's duration averaged over the last
+ * min(calls, n) calls; *count receives the number of kernels.  It
+ * synchronizes on those events. */
+ccl_status ccl_plan_set_profiling(ccl_plan plan, int nsets);
 ccl_status ccl_plan_kernel_times(ccl_plan plan, const char **names, float *ms, int cap,
                                  int *count);
 

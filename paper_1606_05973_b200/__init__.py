@@ -142,11 +142,14 @@ class Plan:
                                       _stream_handle(stream)), "ccl_plan_label_host")
         return out, n_out
 
-    def set_profiling(self, enable=True):
-        _check(_L.ccl_plan_set_profiling(self._p, int(bool(enable))), "ccl_plan_set_profiling")
+    def set_profiling(self, nsets=1):
+        """Record per-kernel CUDA events for the next label() calls (ring of
+        `nsets` calls; 0 disables)."""
+        _check(_L.ccl_plan_set_profiling(self._p, int(nsets)), "ccl_plan_set_profiling")
 
     def kernel_times(self):
-        """{kernel name: ms} of the last profiled label() call (CUDA events on its stream)."""
+        """{kernel name: ms}, averaged over the profiled label() calls in the ring
+        (CUDA events recorded on the launch stream)."""
         cap = 16
         names = (ctypes.c_char_p * cap)()
         ms = (ctypes.c_float * cap)()

@@ -101,10 +101,21 @@ struct ccl_plan_st {
     uint8_t *d_img = nullptr;   // staging buffers for ccl_plan_label_host
     int32_t *d_lab = nullptr;
     int32_t *d_n = nullptr;
-    bool profiling = false;
-    cudaEvent_t ev[K_COUNT + 1] = {};
-    bool have_times = false;
+    int prof_sets = 0;             // profiling ring size (0 = off)
+    cudaEvent_t *ev = nullptr;     // prof_sets * (K_COUNT + 1) events
+    long long prof_calls = 0;      // profiled calls since the ring was (re)armed
 };
+
+static void free_events(ccl_plan p) {
+    if (p->ev) {
+        for (int i = 0; i < p->prof_sets * (K_COUNT + 1); i++)
+            if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+        delete[] p->ev;
+    }
+    p->ev = nullptr;
+    p->prof_sets = 0;
+    p->prof_calls = 0;
+}
 
 static ccl_status check_shape(int H, int W) {
     if (H < 1 || W < 1) return CCL_INVALID_ARGUMENT;
@@ -184,8 +195,7 @@ ccl_status ccl_plan_destroy(ccl_plan p) {
     if (p->d_img) cudaFree(p->d_img);
     if (p->d_lab) cudaFree(p->d_lab);
     if (p->d_n) cudaFree(p->d_n);
-    for (auto &ev : p->ev)
-        if (ev) cudaEventDestroy(ev);
+    free_events(p);
     delete p;
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
 }
@@ -202,13 +212,12 @@ ccl_status ccl_plan_label(ccl_plan p, const uint8_t *img, int32_t *labels, int32
     ccl_status st = check_buffers(img, labels, n_components, p->g.H, p->g.W);
     if (st != CCL_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (p->profiling && !p->ev[0]) {
-        for (auto &ev : p->ev)
-            if (cudaEventCreate(&ev) != cudaSuccess) return CCL_CUDA_ERROR;
+    cudaEvent_t *ev = nullptr;
+    if (p->prof_sets > 0) {
+        ev = p->ev + (p->prof_calls % p->prof_sets) * (K_COUNT + 1);
+        p->prof_calls++;
     }
-    cudaError_t e = run_pipeline(p->g, p->ws, img, labels, n_components, s,
-                                 p->profiling ? p->ev : nullptr);
-    p->have_times = p->profiling;
+    cudaError_t e = run_pipeline(p->g, p->ws, img, labels, n_components, s, ev);
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
 }
 
@@ -234,21 +243,35 @@ ccl_status ccl_plan_label_host(ccl_plan p, const uint8_t *h_img, int32_t *h_labe
     return cudaStreamSynchronize(s) == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
 }
 
-ccl_status ccl_plan_set_profiling(ccl_plan p, int enable) {
-    if (!p) return CCL_INVALID_ARGUMENT;
-    p->profiling = enable != 0;
+ccl_status ccl_plan_set_profiling(ccl_plan p, int nsets) {
+    if (!p || nsets < 0) return CCL_INVALID_ARGUMENT;
+    free_events(p);
+    if (nsets == 0) return CCL_OK;
+    p->ev = new (std::nothrow) cudaEvent_t[(size_t)nsets * (K_COUNT + 1)]();
+    if (!p->ev) return CCL_OUT_OF_MEMORY;
+    p->prof_sets = nsets;
+    for (int i = 0; i < nsets * (K_COUNT + 1); i++)
+        if (cudaEventCreate(&p->ev[i]) != cudaSuccess) return CCL_CUDA_ERROR;
     return CCL_OK;
 }
 
 ccl_status ccl_plan_kernel_times(ccl_plan p, const char **names, float *ms, int cap, int *count) {
     if (!p || !count) return CCL_INVALID_ARGUMENT;
     *count = K_COUNT;
-    if (!p->have_times) return CCL_INVALID_ARGUMENT;
-    if (cudaEventSynchronize(p->ev[K_COUNT]) != cudaSuccess) return CCL_CUDA_ERROR;
+    if (p->prof_sets == 0 || p->prof_calls == 0) return CCL_INVALID_ARGUMENT;
+    const int nset = (int)(p->prof_calls < p->prof_sets ? p->prof_calls : p->prof_sets);
     for (int i = 0; i < K_COUNT && i < cap; i++) {
         if (names) names[i] = kKernelNames[i];
-        if (ms && cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess)
-            return CCL_CUDA_ERROR;
+        if (!ms) continue;
+        double acc = 0;
+        for (int k = 0; k < nset; k++) {
+            cudaEvent_t *e = p->ev + (size_t)k * (K_COUNT + 1);
+            if (cudaEventSynchronize(e[i + 1]) != cudaSuccess) return CCL_CUDA_ERROR;
+            float t = 0;
+            if (cudaEventElapsedTime(&t, e[i], e[i + 1]) != cudaSuccess) return CCL_CUDA_ERROR;
+            acc += t;
+        }
+        ms[i] = (float)(acc / nset);
     }
     return CCL_OK;
 }

@@ -154,12 +154,14 @@ __device__ __forceinline__ int leftmost3(uint32_t w, uint32_t wp, uint32_t wn, i
 
 // ---------------------------------------------------------------- union-find
 // Lock-free Rem's union with splicing on a shared-memory parent array in
-// which parent <= child (labels are created in raster order).  This is the
-// paper's merge with the root link done by atomicCAS (the
-// role of merger's lock + re-check) and the splice by
-// atomicMin (parents only ever decrease, so a splice can never create a cycle).
-__device__ void merge_smem(uint32_t *p, uint32_t x, uint32_t y) {
-    volatile uint32_t *vp = p;
+// which parent < child for every non-root (labels are created in raster
+// order).  This is the paper's merge run concurrently the
+// way its merger does: the root link is an atomicCAS
+// (the role of merger's lock + "still a root?" re-check)
+// and the splice is a plain store, unlocked as in merger (PAPER.md:1025,
+// 1039).  Every value stored into p[x] is smaller than x, so no cycle forms.
+__device__ void merge_smem(uint16_t *p, uint32_t x, uint32_t y) {
+    volatile uint16_t *vp = p;
     while (true) {
         uint32_t px = vp[x], py = vp[y];
         if (px == py) return;
@@ -169,10 +171,12 @@ __device__ void merge_smem(uint32_t *p, uint32_t x, uint32_t y) {
         }
         // now p[x] > p[y]
         if (px == x) {
-            if (atomicCAS(&p[x], x, py) == x) return;
+            if (atomicCAS(reinterpret_cast<unsigned short *>(p + x), (unsigned short)x,
+                          (unsigned short)py) == (unsigned short)x)
+                return;
             continue;  // x stopped being a root meanwhile: retry from x
         }
-        atomicMin(&p[x], py);  // splice: x's subtree becomes a sibling under py
+        vp[x] = (uint16_t)py;  // splice: x's subtree becomes a sibling under py
         x = px;
     }
 }
@@ -232,19 +236,23 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
 
 // ========================================================================= K1
 struct K1Smem {
-    uint32_t p[CAP];               // parent of each provisional label (tile-local index)
-    uint16_t lpos[CAP];            // position (row*1024 + col) of the pixel that created it
-    uint16_t cnode[CAPC];          // border flag, then border index + 1, per component
-    uint16_t lab[NW][3][MAXRUN];   // run labels: 2 ping-pong rows + the strip's first row
+    uint16_t p[CAP];               // parent of each provisional label (tile-local index)
+    uint16_t lpos[CAP];            // position (row*1024 + col) of the pixel that created it;
+                                   // after the flatten, a root's entry holds its component
+    union {
+        uint16_t lab[NW][3][MAXRUN];  // run labels: 2 ping-pong rows + the strip's first row
+        uint16_t cnode[CAPC];         // Phase III: border flag, then border index + 1
+    } u;
     uint32_t hd[NW][3][WPR];       // run heads per lane, same buffers
     uint32_t bs[NW][3][WPR];       // run base per lane, same buffers
     uint32_t bm[TH][WPR];          // the tile's masks
-    int32_t left[TH], right[TH];   // label of the first / last column pixel of each row, -1 bg
+    uint16_t toplab[MAXRUN];       // run labels of the tile's first row
+    uint16_t botlab[MAXRUN];       // run labels of the tile's last row
+    int16_t left[TH], right[TH];   // label of the first / last column pixel of each row, -1 bg
     int32_t used[NW];              // labels created by each strip
     int32_t last[NW];              // buffer holding each strip's last row
     int32_t nrow[NW][2];           // runs in each strip's first / last row
-    int32_t wscan[NW];             // block-scan scratch
-    int32_t total;
+    int32_t wscan[NW];             // scan scratch
 };
 
 // Block-wide exclusive scan of one int per thread (NW warps); returns prefix,
@@ -267,7 +275,23 @@ __device__ __forceinline__ int block_excl_scan(int v, int *scratch, int &total) 
     return pre + off;
 }
 
-__global__ void __launch_bounds__(NW * 32, 2)
+// Upper-side edges that the copy step does not already cover.  With the
+// spanning edge set {(L, leftmost upper of L)} U {(U, leftmost lower of U)},
+// the second family is redundant unless U's head h touches the lower run L
+// through pixel h-1 AND L reaches an upper pixel at h-2 or further left (then
+// L's leftmost upper neighbour is another run).  S is the segmented smear of
+// the touch pixels t along the lower runs (incl. carries from left lanes).
+__device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, uint32_t up,
+                                                      uint32_t x, uint32_t xp, uint32_t S) {
+    const uint32_t Sp = __shfl_up_sync(FULL, S, 1);
+    const uint32_t sp = lane_id() == 0 ? 0u : Sp;
+    const uint32_t x1 = (x << 1) | (xp >> 31);              // lower pixel at h-1
+    const uint32_t s2 = (S << 2) | (sp >> 30);              // smear at h-2
+    const uint32_t u2 = (u << 2) | (up >> 30);              // upper pixel at h-2
+    return hu & x1 & (s2 | u2);
+}
+
+__global__ void __launch_bounds__(NW * 32, 3)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
@@ -290,42 +314,55 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
 
     // ---- Phase I: strip scan, one row at a time (Scan_ARemSP)
     uint32_t next = w * CAPS;  // strip-local label counter (count <- start)
-    uint32_t u = 0, hu = 0, bu = 0;
+    uint32_t u = 0, up = 0, un = 0, hu = 0, bu = 0;
     int prev = 2, cur = 2;
 #pragma unroll
     for (int i = 0; i < S; i++) {
         if (i >= nrows) break;
         const int rl = r0 + i;
         cur = (i == 0) ? 2 : (prev == 0 ? 1 : 0);
-        uint16_t *labc = sm.lab[w][cur];
-        const uint16_t *labp = sm.lab[w][prev];
+        uint16_t *labc = sm.u.lab[w][cur];
+        const uint16_t *labp = sm.u.lab[w][prev];
         const uint32_t x = xs[i];
-        RowView R = make_row(x);
-        sm.hd[w][cur][lane] = R.hx;
-        sm.bs[w][cur][lane] = R.base;
+        const uint32_t xpr = __shfl_up_sync(FULL, x, 1), xnr = __shfl_down_sync(FULL, x, 1);
+        const uint32_t xp = lane == 0 ? 0u : xpr, xn = lane == 31 ? 0u : xnr;
+        const uint32_t hx = x & ~((x << 1) | (xp >> 31));
+
+        // touch pixels: this-row pixels with a foreground pixel among the three above
+        const uint32_t t = x & (u | (u << 1) | (up >> 31) | (u >> 1) | (un << 31));
+        // first touch pixel of each run, and the run smear S (for the merge test)
+        const uint32_t s = smear_up(t, x);
+        const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
+        const uint32_t lead = x & ~(x + 1);
+        const uint32_t S = s | (cin ? lead : 0u);
+        const uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
+        // heads of runs with no touch pixel -> new labels
+        uint32_t nh;
+        {
+            const uint32_t sd = smear_down(t, x);
+            const uint32_t cr = carry_in_bwd((x & sd & 1u) != 0, x == FULL) & (x >> 31);
+            const int k = __clz(~x);
+            const uint32_t trail = k == 0 ? 0u : (k == 32 ? FULL : (FULL << (32 - k)));
+            nh = hx & ~(sd | (cr ? trail : 0u));
+        }
+        // one scan for both run ordinals and new-label numbers
+        uint32_t tot;
+        const uint32_t pre = warp_excl_scan(__popc(hx) | (__popc(nh) << 16), tot);
+        const uint32_t base = pre & 0xFFFFu, nbase = pre >> 16;
+        const uint32_t nr = tot & 0xFFFFu, nnew = tot >> 16;
+        sm.hd[w][cur][lane] = hx;
+        sm.bs[w][cur][lane] = base;
         sm.bm[rl][lane] = x;
         if (gword < g.WW) ws.bm[(int64_t)(R0 + rl) * g.WW + gword] = x;
 
-        // touch pixels: this-row pixels with a foreground pixel among the three above
-        uint32_t up = __shfl_up_sync(FULL, u, 1), un = __shfl_down_sync(FULL, u, 1);
-        up = lane == 0 ? 0u : up;
-        un = lane == 31 ? 0u : un;
-        const uint32_t du = u | (u << 1) | (up >> 31) | (u >> 1) | (un << 31);
-        const uint32_t t = x & du;
-        const uint32_t ft = first_in_run(t, x);
-        const uint32_t nh = untouched_heads(t, R);
-
         // new labels, numbered in column order = raster order
-        uint32_t nnew;
-        uint32_t nbase = warp_excl_scan(__popc(nh), nnew);
         {
             uint32_t m = nh, k = next + nbase;
             while (m) {
-                int b = __ffs(m) - 1;
+                const int b = __ffs(m) - 1;
                 m &= m - 1;
-                int ord = run_ord(R.hx, R.base, b);
-                labc[ord] = (uint16_t)k;
-                sm.p[k] = k;
+                labc[run_ord(hx, base, b)] = (uint16_t)k;
+                sm.p[k] = (uint16_t)k;
                 sm.lpos[k] = (uint16_t)(rl * TW + 32 * lane + b);
                 k++;
             }
@@ -336,46 +373,48 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         {
             uint32_t m = ft;
             while (m) {
-                int b = __ffs(m) - 1;
+                const int b = __ffs(m) - 1;
                 m &= m - 1;
-                int q = 32 * lane + b + leftmost3(u, up, un, b);
-                int lq = q >> 5;
-                int ou = run_ord(sm.hd[w][prev][lq], sm.bs[w][prev][lq], q & 31);
-                labc[run_ord(R.hx, R.base, b)] = labp[ou];
+                const int q = 32 * lane + b + leftmost3(u, up, un, b);
+                const int lq = q >> 5;
+                const int ou = run_ord(sm.hd[w][prev][lq], sm.bs[w][prev][lq], q & 31);
+                labc[run_ord(hx, base, b)] = labp[ou];
             }
         }
         __syncwarp();
-        // merge: every upper run with the lower run its first contact pixel
-        // touches; only differing labels need a union
+        // merge: the few upper runs whose lower neighbour copied another
+        // label (the decision tree's copy(c,a)/copy(c,d) merges)
         if (i > 0) {
-            const uint32_t tu = u & dilate(R);
-            uint32_t m = first_in_run(tu, u);
+            uint32_t m = upper_merge_heads(hu, u, up, x, xp, S);
             while (m) {
-                int b = __ffs(m) - 1;
+                const int b = __ffs(m) - 1;
                 m &= m - 1;
-                int q = 32 * lane + b + leftmost3(x, R.xp, R.xn, b);
-                int lq = q >> 5;
-                uint32_t lx = labc[run_ord(sm.hd[w][cur][lq], sm.bs[w][cur][lq], q & 31)];
-                uint32_t lu = labp[run_ord(hu, bu, b)];
+                const int q = 32 * lane + b - 1;  // lower pixel h-1 of the run below
+                const int lq = q >> 5;
+                const uint32_t lx = labc[run_ord(sm.hd[w][cur][lq], sm.bs[w][cur][lq], q & 31)];
+                const uint32_t lu = labp[run_ord(hu, bu, b)];
                 if (lx != lu) merge_smem(sm.p, lu, lx);
             }
         }
         // per-row outputs: run labels (for K5) and the border-column labels
         {
-            uint16_t *dst = ws.runlab + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
-            for (int k = lane; k < (int)R.nr; k += 32) dst[k] = labc[k];
-            if (lane == 0) sm.left[rl] = (x & 1u) ? (int)labc[0] : -1;
+            uint32_t *dst = reinterpret_cast<uint32_t *>(ws.runlab + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN);
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(labc);
+            for (int k = lane; 2 * k < (int)nr; k += 32) dst[k] = src[k];
+            if (lane == 0) sm.left[rl] = (x & 1u) ? (int16_t)labc[0] : (int16_t)-1;
             const int lc = vcols - 1;
-            if (lane == (lc >> 5)) sm.right[rl] = ((x >> (lc & 31)) & 1u) ? (int)labc[R.nr - 1] : -1;
+            if (lane == (lc >> 5)) sm.right[rl] = ((x >> (lc & 31)) & 1u) ? (int16_t)labc[nr - 1] : (int16_t)-1;
             if (lane == 0) {
-                if (i == 0) sm.nrow[w][0] = (int)R.nr;
-                sm.nrow[w][1] = (int)R.nr;
+                if (i == 0) sm.nrow[w][0] = (int)nr;
+                sm.nrow[w][1] = (int)nr;
             }
         }
         __syncwarp();
         u = x;
-        hu = R.hx;
-        bu = R.base;
+        up = xp;
+        un = xn;
+        hu = hx;
+        bu = base;
         prev = cur;
     }
     if (lane == 0) {
@@ -389,118 +428,128 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     if (w > 0 && r0 < rows) {
         const int pw = w - 1, pb = sm.last[pw];
         const uint32_t uu = sm.bm[r0 - 1][lane], x = sm.bm[r0][lane];
-        const uint16_t *labu = sm.lab[pw][pb];
-        const uint16_t *labx = sm.lab[w][2];
+        const uint16_t *labu = sm.u.lab[pw][pb];
+        const uint16_t *labx = sm.u.lab[w][2];
         const uint32_t *hdu = sm.hd[pw][pb], *bsu = sm.bs[pw][pb];
         const uint32_t *hdx = sm.hd[w][2], *bsx = sm.bs[w][2];
         RowView X = make_row(x);
         RowView U = make_row(uu);
         const uint32_t t = x & dilate(U);
-        uint32_t m = first_in_run(t, x);
+        const uint32_t s = smear_up(t, x);
+        const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
+        const uint32_t lead = x & ~(x + 1);
+        const uint32_t S = s | (cin ? lead : 0u);
+        uint32_t m = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
         while (m) {  // each lower run with its leftmost upper neighbour
-            int b = __ffs(m) - 1;
+            const int b = __ffs(m) - 1;
             m &= m - 1;
-            int q = 32 * lane + b + leftmost3(uu, U.xp, U.xn, b);
-            int lq = q >> 5;
-            uint32_t lu = labu[run_ord(hdu[lq], bsu[lq], q & 31)];
-            uint32_t lx = labx[run_ord(X.hx, X.base, b)];
+            const int q = 32 * lane + b + leftmost3(uu, U.xp, U.xn, b);
+            const int lq = q >> 5;
+            const uint32_t lu = labu[run_ord(hdu[lq], bsu[lq], q & 31)];
+            const uint32_t lx = labx[run_ord(X.hx, X.base, b)];
             if (lx != lu) merge_smem(sm.p, lu, lx);
         }
-        const uint32_t tu = uu & dilate(X);
-        m = first_in_run(tu, uu);
-        while (m) {  // each upper run with its leftmost lower neighbour
-            int b = __ffs(m) - 1;
+        m = upper_merge_heads(U.hx, uu, U.xp, x, X.xp, S);
+        while (m) {  // upper runs whose leftmost lower neighbour has another leftmost upper
+            const int b = __ffs(m) - 1;
             m &= m - 1;
-            int q = 32 * lane + b + leftmost3(x, X.xp, X.xn, b);
-            int lq = q >> 5;
-            uint32_t lx = labx[run_ord(hdx[lq], bsx[lq], q & 31)];
-            uint32_t lu = labu[run_ord(U.hx, U.base, b)];
+            const int q = 32 * lane + b - 1;
+            const int lq = q >> 5;
+            const uint32_t lx = labx[run_ord(hdx[lq], bsx[lq], q & 31)];
+            const uint32_t lu = labu[run_ord(U.hx, U.base, b)];
             if (lx != lu) merge_smem(sm.p, lu, lx);
         }
+    }
+    // keep the tile's first and last row labels (the lab buffers are reused below)
+    const int wl = (rows - 1) / S;  // strip holding the tile's last row
+    if (w == 0) {
+        const uint16_t *src = sm.u.lab[0][2];
+        for (int k = lane; k < sm.nrow[0][0]; k += 32) sm.toplab[k] = src[k];
+    }
+    if (w == wl) {
+        const uint16_t *src = sm.u.lab[wl][sm.last[wl]];
+        for (int k = lane; k < sm.nrow[wl][1]; k += 32) sm.botlab[k] = src[k];
     }
     __syncthreads();
 
     // ---- Phase III: tile flatten: roots in label order
-    // (= raster order of first pixel) get consecutive component indices.
-    int used[NW], ubase[NW];
-    int ntot = 0;
-#pragma unroll
-    for (int i = 0; i < NW; i++) {
-        used[i] = sm.used[i];
-        ubase[i] = ntot;
-        ntot += used[i];
-    }
-    auto label_of = [&](int d) -> int {
-        int s = 0;
-#pragma unroll
-        for (int i = 1; i < NW; i++) s += d >= ubase[i] ? 1 : 0;
-        return s * CAPS + (d - ubase[s]);
-    };
+    // (= raster order of the creating pixel) get consecutive component
+    // indices.  Warp w walks its own strip's labels in order.
+    const int used_w = sm.used[w];
+    const int lbase = w * CAPS;
+    volatile uint16_t *vp = sm.p;
     // (a) full path compression
-    for (int d = threadIdx.x; d < ntot; d += NW * 32) {
-        int l = label_of(d);
-        volatile uint32_t *vp = sm.p;
+    for (int i = lane; i < used_w; i += 32) {
+        const int l = lbase + i;
         uint32_t r = vp[l];
         while (vp[r] != r) r = vp[r];
-        vp[l] = r;
+        vp[l] = (uint16_t)r;
     }
     __syncthreads();
-    // (b) roots -> component index, key of the first pixel
-    const int per = (ntot + NW * 32 - 1) / (NW * 32);
-    const int d0 = threadIdx.x * per, d1 = min(ntot, d0 + per);
-    int cnt = 0;
-    for (int d = d0; d < d1; d++) {
-        int l = label_of(d);
-        cnt += sm.p[l] == (uint32_t)l;
+    // (b) count roots per strip, then number them in label order
+    int nroot = 0;
+    for (int i0 = 0; i0 < used_w; i0 += 32) {
+        const int i = i0 + lane;
+        nroot += __popc(__ballot_sync(FULL, i < used_w && sm.p[lbase + i] == (uint16_t)(lbase + i)));
     }
-    int ncomp;
-    int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
+    if (lane == 0) sm.wscan[w] = nroot;
+    __syncthreads();
+    int coff = 0, ncomp = 0;
+#pragma unroll
+    for (int k = 0; k < NW; k++) {
+        const int v = sm.wscan[k];
+        coff += k < w ? v : 0;
+        ncomp += v;
+    }
     int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
-    for (int d = d0; d < d1; d++) {
-        int l = label_of(d);
-        if (sm.p[l] == (uint32_t)l) {
-            int pos = sm.lpos[l];
-            compkey[cidx] = (R0 + (pos >> 10)) * g.W + C0 + (pos & (TW - 1));
-            sm.lpos[l] = (uint16_t)cidx;  // lpos of a root now holds its component
-            cidx++;
+    for (int i0 = 0; i0 < used_w; i0 += 32) {
+        const int i = i0 + lane;
+        const int l = lbase + i;
+        const bool root = i < used_w && sm.p[l] == (uint16_t)l;
+        const uint32_t bal = __ballot_sync(FULL, root);
+        if (root) {
+            const int c = coff + __popc(bal & ((1u << lane) - 1));
+            const int pos = sm.lpos[l];
+            compkey[c] = (R0 + (pos >> 10)) * g.W + C0 + (pos & (TW - 1));
+            sm.lpos[l] = (uint16_t)c;  // a root's lpos now holds its component
         }
+        coff += __popc(bal);
     }
-    for (int c = threadIdx.x; c < ncomp; c += NW * 32) sm.cnode[c] = 0;
     __syncthreads();
-    // (c) provisional label -> component (for K5)
+    // (c) provisional label -> component (for K5); clear the border flags
     uint16_t *lmap = ws.lmap + (int64_t)tile * CAP;
-    for (int d = threadIdx.x; d < ntot; d += NW * 32) {
-        int l = label_of(d);
+    for (int i = lane; i < used_w; i += 32) {
+        const int l = lbase + i;
         lmap[l] = sm.lpos[sm.p[l]];
     }
+    for (int c = threadIdx.x; c < ncomp; c += NW * 32) sm.u.cnode[c] = 0;
+    __syncthreads();
     // (d) mark components that touch the tile border
     auto comp_of = [&](int l) -> int { return sm.lpos[sm.p[l]]; };
-    const int wl = (rows - 1) / S;  // strip holding the tile's last row
     const int ntop = sm.nrow[0][0], nbot = sm.nrow[wl][1];
-    const uint16_t *labtop = sm.lab[0][2], *labbot = sm.lab[wl][sm.last[wl]];
-    for (int k = threadIdx.x; k < ntop; k += NW * 32) sm.cnode[comp_of(labtop[k])] = 1;
-    for (int k = threadIdx.x; k < nbot; k += NW * 32) sm.cnode[comp_of(labbot[k])] = 1;
+    for (int k = threadIdx.x; k < ntop; k += NW * 32) sm.u.cnode[comp_of(sm.toplab[k])] = 1;
+    for (int k = threadIdx.x; k < nbot; k += NW * 32) sm.u.cnode[comp_of(sm.botlab[k])] = 1;
     for (int r = threadIdx.x; r < rows; r += NW * 32) {
-        if (sm.left[r] >= 0) sm.cnode[comp_of(sm.left[r])] = 1;
-        if (sm.right[r] >= 0) sm.cnode[comp_of(sm.right[r])] = 1;
+        if (sm.left[r] >= 0) sm.u.cnode[comp_of(sm.left[r])] = 1;
+        if (sm.right[r] >= 0) sm.u.cnode[comp_of(sm.right[r])] = 1;
     }
     __syncthreads();
     // (e) border components -> global union-find nodes
     const int cper = (ncomp + NW * 32 - 1) / (NW * 32);
     const int c0 = threadIdx.x * cper, c1 = min(ncomp, c0 + cper);
     int bc = 0;
-    for (int c = c0; c < c1; c++) bc += sm.cnode[c] != 0;
+    for (int c = c0; c < c1; c++) bc += sm.u.cnode[c] != 0;
     int nborder;
     int bidx = block_excl_scan(bc, sm.wscan, nborder);
     int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
     const int nodebase = tile * CAPB;
     for (int c = c0; c < c1; c++) {
-        if (sm.cnode[c]) {
-            int node = nodebase + bidx;
+        if (sm.u.cnode[c]) {
+            const int node = nodebase + bidx;
             compnode[c] = node;
             ws.gparent[node] = node;
             ws.gkey[node] = compkey[c];
-            sm.cnode[c] = (uint16_t)(bidx + 1);
+            sm.u.cnode[c] = (uint16_t)(bidx + 1);
             bidx++;
         } else {
             compnode[c] = -1;
@@ -508,11 +557,11 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     }
     __syncthreads();
     // (f) nodes of the border pixels, for K2
-    auto node_of = [&](int l) -> int { return nodebase + (int)sm.cnode[comp_of(l)] - 1; };
-    for (int k = threadIdx.x; k < ntop; k += NW * 32) ws.topnode[tile * MAXRUN + k] = node_of(labtop[k]);
-    for (int k = threadIdx.x; k < nbot; k += NW * 32) ws.botnode[tile * MAXRUN + k] = node_of(labbot[k]);
+    auto node_of = [&](int l) -> int { return nodebase + (int)sm.u.cnode[comp_of(l)] - 1; };
+    for (int k = threadIdx.x; k < ntop; k += NW * 32) ws.topnode[tile * MAXRUN + k] = node_of(sm.toplab[k]);
+    for (int k = threadIdx.x; k < nbot; k += NW * 32) ws.botnode[tile * MAXRUN + k] = node_of(sm.botlab[k]);
     for (int r = threadIdx.x; r < rows; r += NW * 32) {
-        int64_t o = (int64_t)tx * g.H + R0 + r;
+        const int64_t o = (int64_t)tx * g.H + R0 + r;
         ws.leftnode[o] = sm.left[r] >= 0 ? node_of(sm.left[r]) : -1;
         ws.rightnode[o] = sm.right[r] >= 0 ? node_of(sm.right[r]) : -1;
     }
@@ -522,7 +571,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         meta[META_NBORDER] = nborder;
         meta[META_ROWS] = rows;
     }
-    if (threadIdx.x < NW) ws.meta[(int64_t)tile * META + META_USED + threadIdx.x] = used[threadIdx.x];
+    if (lane == 0) ws.meta[(int64_t)tile * META + META_USED + w] = used_w;
 }
 
 // ========================================================================= K2
@@ -719,9 +768,21 @@ k_scan(Geometry g, Workspace ws, int32_t *n_components) {
 
 // ========================================================================= K5
 struct K5Smem {
-    int32_t clab[CAPC];          // component -> final label; later reused as row label buffers
     int32_t flab[CAP];           // provisional label -> final label
+    int32_t rowbuf[NW][TW];      // per-warp row staging (run labels, then the swizzled output row)
 };
+
+// Final label of a tile component (flatten's consecutive numbering,
+// PAPER.md:714-715, in raster order): roots from their segment offset and
+// rank; border components that are not roots from their global root's.
+__device__ __forceinline__ int32_t comp_label(const Geometry &g, const Workspace &ws, int tile,
+                                              int R0, int tx, int c) {
+    const uint32_t cr = ws.comprank[(int64_t)tile * CAPC + c];
+    if (cr != 0xFFFFFFFFu)
+        return ws.segoff[(int64_t)(R0 + (int)(cr >> 16)) * g.nTx + tx] + (int)(cr & 0xFFFF) + 1;
+    const int root = gfind_ro(ws.gparent, ws.compnode[(int64_t)tile * CAPC + c]);
+    return ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+}
 
 __global__ void __launch_bounds__(NW * 32, 3)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
@@ -732,71 +793,72 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const int tx = tile % g.nTx, ty = tile / g.nTx;
     const int R0 = ty * TH, C0 = tx * TW;
     const int32_t *meta = ws.meta + (int64_t)tile * META;
-    const int ncomp = meta[META_NCOMP], rows = meta[META_ROWS];
+    const int rows = meta[META_ROWS];
+    const int vcols = min(TW, g.W - C0);
+    const int gword = tx * WPR + lane;
 
-    // component labels (flatten's final numbering)
-    const uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
-    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
-    for (int c = threadIdx.x; c < ncomp; c += NW * 32) {
-        uint32_t cr = comprank[c];
-        int lab;
-        if (cr != 0xFFFFFFFFu) {
-            lab = ws.segoff[(int64_t)(R0 + (int)(cr >> 16)) * g.nTx + tx] + (int)(cr & 0xFFFF) + 1;
-        } else {
-            int root = gfind_ro(ws.gparent, compnode[c]);
-            lab = ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
-        }
-        sm.clab[c] = lab;
+    // this warp's rows are w, w+NW, ...; the next row's mask is always in flight
+    auto load_mask = [&](int rl) -> uint32_t {
+        return (rl < rows && gword < g.WW) ? __ldcs(ws.bm + (int64_t)(R0 + rl) * g.WW + gword) : 0u;
+    };
+    uint32_t xnext = load_mask(w);
+    // provisional label -> final label (warp w: strip w's labels)
+    {
+        const int used = meta[META_USED + w];
+        const uint16_t *lmap = ws.lmap + (int64_t)tile * CAP + w * CAPS;
+        for (int i = lane; i < used; i += 32)
+            sm.flab[w * CAPS + i] = comp_label(g, ws, tile, R0, tx, lmap[i]);
     }
     __syncthreads();
-    const uint16_t *lmap = ws.lmap + (int64_t)tile * CAP;
-    for (int s = 0; s < NW; s++) {
-        const int used = meta[META_USED + s];
-        for (int i = threadIdx.x; i < used; i += NW * 32) {
-            int l = s * CAPS + i;
-            sm.flab[l] = sm.clab[lmap[l]];
-        }
-    }
-    __syncthreads();
-    int32_t *rowlab = sm.clab + w * MAXRUN;  // per-warp run labels of the current row
 
-    for (int rl = w; rl < rows; rl += NW) {
+    int32_t *buf = sm.rowbuf[w];
+    int32_t *rowlab = buf + MAXRUN;  // upper half: run labels of the current row
+#pragma unroll 1
+    for (int i = 0; i < TH / NW; i++) {
+        const int rl = w + i * NW;
+        if (rl >= rows) break;
         const int row = R0 + rl;
-        const int gword = tx * WPR + lane;
-        const uint32_t x = gword < g.WW ? ws.bm[(int64_t)row * g.WW + gword] : 0u;
+        const uint32_t x = xnext;
+        xnext = load_mask(rl + NW);
         const uint32_t xl = __shfl_up_sync(FULL, x, 1);
         const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
         uint32_t nr;
         const uint32_t base = warp_excl_scan(__popc(hx), nr);
         const uint16_t *rlab = ws.runlab + ((int64_t)row * g.nTx + tx) * MAXRUN;
-        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = sm.flab[rlab[k]];
+        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = sm.flab[__ldcs(rlab + k)];
+        __syncwarp();
+        // walk this lane's 32 pixels: the label changes only at run heads
+        int v[32];
+        {
+            int ord = (int)base;
+            int cur = ((x & 1u) && !(hx & 1u)) ? rowlab[ord - 1] : 0;
+#pragma unroll
+            for (int b = 0; b < 32; b++) {
+                if ((hx >> b) & 1u) cur = rowlab[ord++];
+                v[b] = ((x >> b) & 1u) ? cur : 0;
+            }
+        }
+        __syncwarp();
+        // stage the row: lane's 32 labels = 8 16-byte chunks, XOR-swizzled so
+        // both the row-wise writes and the coalesced reads are conflict-free
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            *reinterpret_cast<int4 *>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                make_int4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
         int32_t *out = labels + (int64_t)row * g.W + C0;
 #pragma unroll
         for (int c = 0; c < 8; c++) {
-            const int wi = 4 * c + (lane >> 3);
-            const uint32_t xw = __shfl_sync(FULL, x, wi);
-            const uint32_t hw = __shfl_sync(FULL, hx, wi);
-            const uint32_t bw = __shfl_sync(FULL, base, wi);
-            const int b0 = 4 * (lane & 7);
-            const int col = 128 * c + 4 * lane;
-            int v[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int b = b0 + k;
-                v[k] = ((xw >> b) & 1u) ? rowlab[run_ord(hw, bw, b)] : 0;
-            }
-#ifdef CCL_DEBUG_PRINT
-            if (lane < 2 && c == 0)
-                printf("K5 tile %d row %d lane %d x=%x hx=%x base=%u nr=%u xw=%x v=%d %d %d %d rowlab0=%d flab0=%d clab?\n",
-                       tile, row, lane, x, hx, base, nr, xw, v[0], v[1], v[2], v[3], rowlab[0], sm.flab[0]);
-#endif
+            const int P = 128 * c + 4 * lane;          // first pixel of this lane's chunk
+            const int jw = P >> 5, jj = (P >> 2) & 7;  // source lane-word and chunk
+            const int4 o = *reinterpret_cast<const int4 *>(buf + jw * 32 + ((jj ^ (jw & 7)) << 2));
             if (g.aligned) {
-                if (C0 + col < g.W) __stcs(reinterpret_cast<int4 *>(out + col), make_int4(v[0], v[1], v[2], v[3]));
+                if (P < vcols) __stcs(reinterpret_cast<int4 *>(out + P), o);
             } else {
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (C0 + col + k < g.W) __stcs(out + col + k, v[k]);
+                if (P < vcols) __stcs(out + P, o.x);
+                if (P + 1 < vcols) __stcs(out + P + 1, o.y);
+                if (P + 2 < vcols) __stcs(out + P + 2, o.z);
+                if (P + 3 < vcols) __stcs(out + P + 3, o.w);
             }
         }
         __syncwarp();
