@@ -28,7 +28,7 @@ METRIC = "8-conn CCL Gpixel/s on 21600² image at 1/2/4/8 B200; % of HBM rooflin
 WORKLOAD = "c4_voronoi_21600"
 # algorithmic bytes per pixel: 1 B image read + 4 B label write
 ALG_BYTES_PER_PX = {"path": 5, "k_tile_local": 1, "k_write": 4,
-                    "k_border": 0, "k_roots": 0, "k_scan": 0}
+                    "k_border": 0, "k_roots": 0, "k_scan": 0, "k_final": 0}
 
 
 def parse_args():
@@ -205,8 +205,9 @@ def main():
     if ws == 1:
         plan = ccl.Plan(H, W, device=dev)
         step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
-        nT = ((W + 1023) // 1024) * ((H + 31) // 32)
-        launches_per_step = 5 if nT > 1 else 4
+        nTx, nTy = (W + 1023) // 1024, (H + 31) // 32
+        # mirrors cclb::pipeline_launches: k_border only runs when tiles have neighbours
+        launches_per_step = 5 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
     else:
         uid = ccl.nccl_unique_id() if rank == 0 else None
         obj = [uid]

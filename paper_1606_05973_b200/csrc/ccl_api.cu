@@ -26,7 +26,7 @@ Geometry make_geometry(int H, int W) {
 }
 
 enum {
-    A_BM, A_RUNLAB, A_LMAP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_GPARENT, A_GKEY, A_GNODESEG,
+    A_BM, A_RUNCOMP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODESEG,
     A_GNODERANK, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE,
     A_TICKET, A_COUNT
 };
@@ -35,11 +35,11 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
     const size_t nT = (size_t)g.nT, H = (size_t)g.H;
     const size_t sz[A_COUNT] = {
         H * g.WW * 4,                   // bm
-        H * g.nTx * MAXRUN * 2,         // runlab
-        nT * CAP * 2,                   // lmap
+        H * g.nTx * MAXRUN * 2,         // runcomp
         nT * CAPC * 4,                  // compkey
         nT * CAPC * 4,                  // compnode
         nT * CAPC * 4,                  // comprank
+        nT * CAPC * 4,                  // complab
         nT * CAPB * 4,                  // gparent
         nT * CAPB * 4,                  // gkey
         nT * CAPB * 4,                  // gnodeseg
@@ -68,11 +68,11 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     char *b = static_cast<char *>(base);
     Workspace w;
     w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
-    w.runlab = reinterpret_cast<uint16_t *>(b + offs[A_RUNLAB]);
-    w.lmap = reinterpret_cast<uint16_t *>(b + offs[A_LMAP]);
+    w.runcomp = reinterpret_cast<uint16_t *>(b + offs[A_RUNCOMP]);
     w.compkey = reinterpret_cast<int32_t *>(b + offs[A_COMPKEY]);
     w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);
     w.comprank = reinterpret_cast<uint32_t *>(b + offs[A_COMPRANK]);
+    w.complab = reinterpret_cast<int32_t *>(b + offs[A_COMPLAB]);
     w.gparent = reinterpret_cast<int32_t *>(b + offs[A_GPARENT]);
     w.gkey = reinterpret_cast<int32_t *>(b + offs[A_GKEY]);
     w.gnodeseg = reinterpret_cast<int32_t *>(b + offs[A_GNODESEG]);

@@ -9,19 +9,17 @@ namespace cclb {
 // ---- tiling ------------------------------------
 constexpr int TW = 1024;               // tile width in pixels: one warp-row, 32 lanes x 32 bits
 constexpr int WPR = TW / 32;           // 32-bit words per tile row
-constexpr int NW = 8;                  // warps per CTA (K1, K5)
-constexpr int S = 4;                   // rows per strip; warp w scans rows [w*S, w*S+S) in order
+constexpr int NW = 8;                  // warps per K1 CTA
+constexpr int S = 4;                   // rows per warp in K1
 constexpr int TH = NW * S;             // tile height (32)
 constexpr int MAXRUN = TW / 2;         // max runs in one tile row
-// New provisional labels are created only at run heads with no foreground in
-// the row above (within the strip); such heads are pairwise non-adjacent in
-// the king's graph, so a strip creates at most ceil(S/2)*ceil(TW/2) labels.
-constexpr int CAPS = ((S + 1) / 2) * (TW / 2);
-constexpr int CAP = NW * CAPS;         // provisional labels per tile (8192 < 65536: u16)
-constexpr int CAPC = CAP;              // tile-local components per tile
+constexpr int RCAP = TH * MAXRUN;      // max runs in one tile (16384 < 2^15)
+// Components of a tile are at most its largest set of pairwise non-adjacent
+// pixels (king's graph): ceil(TH/2) * ceil(TW/2).
+constexpr int CAPC = (TH / 2) * (TW / 2);
 constexpr int CAPB = 2 * MAXRUN + TH;  // components touching the tile border
-constexpr int META = 16;               // ints of per-tile metadata
-constexpr int META_NCOMP = 0, META_NBORDER = 1, META_ROWS = 2, META_USED = 4;  // USED..USED+NW
+constexpr int META = 4;                // ints of per-tile metadata
+constexpr int META_NCOMP = 0, META_NBORDER = 1, META_ROWS = 2;
 
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
@@ -40,11 +38,11 @@ struct Geometry {
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
-    uint16_t *runlab;     // [H][nTx][MAXRUN]  provisional label of each run of each tile row
-    uint16_t *lmap;       // [nT][CAP]         provisional label -> tile-local component
+    uint16_t *runcomp;    // [H][nTx][MAXRUN]  tile component of each run of each tile row
     int32_t *compkey;     // [nT][CAPC]        raster index of the component's first pixel
     int32_t *compnode;    // [nT][CAPC]        border-node id, or -1 (component inside the tile)
     uint32_t *comprank;   // [nT][CAPC]        (row<<16 | rank within its segment) for global roots
+    int32_t *complab;     // [nT][CAPC]        final label of the component
     int32_t *gparent;     // [nT][CAPB]        global union-find over border components
     int32_t *gkey;        // [nT][CAPB]        raster key of the node's first pixel
     int32_t *gnodeseg;    // [nT][CAPB]        segment of a root node's first pixel
@@ -65,7 +63,7 @@ Geometry make_geometry(int H, int W);
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 
-enum { K_TILE = 0, K_BORDER, K_ROOTS, K_SCAN, K_WRITE, K_COUNT };
+enum { K_TILE = 0, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it
@@ -73,5 +71,7 @@ extern const char *const kKernelNames[K_COUNT];
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev);
+// Number of kernel launches run_pipeline makes for this geometry.
+int pipeline_launches(const Geometry &g);
 
 }  // namespace cclb

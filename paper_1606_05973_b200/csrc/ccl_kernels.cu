@@ -1,29 +1,26 @@
 // ccl_kernels.cu -- B200 (sm_100a) kernels of the two-pass 8-connectivity CCL
 // pipeline.  DESIGN.md explains the design; paper citations are PAPER.md lines.
 //
-//   K1 k_tile_local   one CTA per 32x1024 tile.  Loads the image tile (128-bit
-//                     streaming loads), packs it into 32-bit row masks, and
-//                     labels it with the paper's two-pass scheme in shared
-//                     memory: 8 warps each scan a 4-row strip row by row
-//                     (Scan_ARemSP's "copy the label of an upper neighbour,
-//                     else a new label, merge the rest"),
-//                     working on whole runs with ballots/popc instead of
-//                     pixels; strips are then merged at their boundary rows
-//                     (PARemSP's boundary loop) with a
-//                     lock-free Rem's union with splicing (merge / merger,
-//                     PAPER.md:669-698, 1001-1046); a tile-level flatten
-//                      numbers the tile's components in
-//                     raster order of their first pixel.
+//   K1 k_tile_local   one CTA per 32x1024 tile.  128-bit streaming loads of the
+//                     image, packed into 32-bit row masks; the runs of the tile
+//                     are its provisional labels (index order = raster order).
+//                     Scan: every run hooks to its leftmost upper neighbour
+//                     (Scan_ARemSP's copy), all rows at once;
+//                     flatten of the hooks in increasing order;
+//                     the few remaining edges merged with a lock-free Rem's
+//                     union with splicing (merge / merger, PAPER.md:669-698,
+//                     1001-1046); roots numbered in raster order.
 //   K2 k_border       lock-free atomicCAS union of the components that touch
-//                     across tile edges (PARemSP's boundary merge, with CAS in
-//                     place of omp locks).
+//                     across tile edges (PARemSP's boundary merge, PAPER.md:971-988,
+//                     with CAS in place of omp locks).
 //   K3 k_roots        per tile: which components are global roots, and their
 //                     rank inside their (row, tile-column) segment.
 //   K4 k_scan         hand-written decoupled-lookback exclusive scan of the
 //                     per-segment root counts = flatten's consecutive numbering
 //                     k++  in raster order; writes N.
+//   K4b k_final       final label of every tile component.
 //   K5 k_write        labeling phase: every pixel gets its
-//                     component's canonical label; 16-byte streaming stores.
+//                     component's label; coalesced 16-byte streaming stores.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -35,7 +32,7 @@ namespace cclb {
 #define FULL 0xFFFFFFFFu
 
 const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_roots", "k_scan",
-                                           "k_write"};
+                                           "k_final", "k_write"};
 
 // ===================================================================== helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -235,24 +232,19 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
 }
 
 // ========================================================================= K1
+// Tile-local two-pass labeling with runs as the provisional labels.  A run's
+// index k (row-major over the tile) plays the role of ARemSP's provisional
+// label: indices grow in raster order of the runs' heads, so "link to the
+// smaller index" keeps every root at its component's first pixel.
 struct K1Smem {
-    uint16_t p[CAP];               // parent of each provisional label (tile-local index)
-    uint16_t lpos[CAP];            // position (row*1024 + col) of the pixel that created it;
-                                   // after the flatten, a root's entry holds its component
-    union {
-        uint16_t lab[NW][3][MAXRUN];  // run labels: 2 ping-pong rows + the strip's first row
-        uint16_t cnode[CAPC];         // Phase III: border flag, then border index + 1
-    } u;
-    uint32_t hd[NW][3][WPR];       // run heads per lane, same buffers
-    uint32_t bs[NW][3][WPR];       // run base per lane, same buffers
-    uint32_t bm[TH][WPR];          // the tile's masks
-    uint16_t toplab[MAXRUN];       // run labels of the tile's first row
-    uint16_t botlab[MAXRUN];       // run labels of the tile's last row
-    int16_t left[TH], right[TH];   // label of the first / last column pixel of each row, -1 bg
-    int32_t used[NW];              // labels created by each strip
-    int32_t last[NW];              // buffer holding each strip's last row
-    int32_t nrow[NW][2];           // runs in each strip's first / last row
-    int32_t wscan[NW];             // scan scratch
+    uint16_t p[RCAP];              // parent of each run (the union-find array p of Alg. merge)
+    uint32_t bm[TH][WPR];          // row masks
+    uint32_t hd[TH][WPR];          // run heads per lane word
+    uint32_t mc[TH][WPR];          // upper-side merge heads per lane word
+    uint16_t hbase[TH][WPR];       // runs whose head lies in earlier words of the row
+    int32_t nrun[TH];              // runs per row
+    int32_t rowbase[TH + 1];       // runs in earlier rows
+    int32_t wscan[NW];             // block-scan scratch
 };
 
 // Block-wide exclusive scan of one int per thread (NW warps); returns prefix,
@@ -275,12 +267,13 @@ __device__ __forceinline__ int block_excl_scan(int v, int *scratch, int &total) 
     return pre + off;
 }
 
-// Upper-side edges that the copy step does not already cover.  With the
-// spanning edge set {(L, leftmost upper of L)} U {(U, leftmost lower of U)},
-// the second family is redundant unless U's head h touches the lower run L
-// through pixel h-1 AND L reaches an upper pixel at h-2 or further left (then
-// L's leftmost upper neighbour is another run).  S is the segmented smear of
-// the touch pixels t along the lower runs (incl. carries from left lanes).
+// Upper-side edges that the hook step does not already cover.  The edge set
+// {(L, leftmost upper run of L)} U {(U, leftmost lower run of U)} connects
+// everything two adjacent rows connect; the second family is redundant unless
+// U's head h touches the lower run L through pixel h-1 AND L reaches an upper
+// pixel at h-2 or further left (then L's leftmost upper neighbour is another
+// run).  S is the segmented smear of the touch pixels along the lower runs,
+// including carries from the lanes to the left.
 __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, uint32_t up,
                                                       uint32_t x, uint32_t xp, uint32_t S) {
     const uint32_t Sp = __shfl_up_sync(FULL, S, 1);
@@ -291,7 +284,11 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
     return hu & x1 & (s2 | u2);
 }
 
-__global__ void __launch_bounds__(NW * 32, 3)
+__device__ __forceinline__ int run_index(const K1Smem &sm, int r, int lane_word, int bit) {
+    return sm.rowbase[r] + sm.hbase[r][lane_word] + __popc(sm.hd[r][lane_word] & upto(bit)) - 1;
+}
+
+__global__ void __launch_bounds__(NW * 32, 4)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
@@ -303,267 +300,200 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     const int rows = min(TH, g.H - R0);
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;  // this lane's word index in the image row
-    const int col0 = C0 + 32 * lane;
-
-    // ---- load this strip's rows (all loads in flight together)
     const int r0 = w * S;
-    const int nrows = max(0, min(S, rows - r0));
-    uint32_t xs[S];
-#pragma unroll
-    for (int i = 0; i < S; i++) xs[i] = i < nrows ? load_word(img, g, R0 + r0 + i, col0) : 0u;
 
-    // ---- Phase I: strip scan, one row at a time (Scan_ARemSP)
-    uint32_t next = w * CAPS;  // strip-local label counter (count <- start)
-    uint32_t u = 0, up = 0, un = 0, hu = 0, bu = 0;
-    int prev = 2, cur = 2;
+    // ---- P0: image -> row masks, run heads, per-word run counts
+    {
+        uint32_t xs[S];
+#pragma unroll
+        for (int i = 0; i < S; i++) xs[i] = (r0 + i < rows) ? load_word(img, g, R0 + r0 + i, C0 + 32 * lane) : 0u;
+#pragma unroll
+        for (int i = 0; i < S; i++) {
+            const int rl = r0 + i;
+            const uint32_t x = xs[i];
+            const uint32_t xl = __shfl_up_sync(FULL, x, 1);
+            const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
+            uint32_t nr;
+            const uint32_t base = warp_excl_scan(__popc(hx), nr);
+            sm.bm[rl][lane] = x;
+            sm.hd[rl][lane] = hx;
+            sm.hbase[rl][lane] = (uint16_t)base;
+            if (lane == 0) sm.nrun[rl] = (int)nr;
+            if (rl < rows && gword < g.WW) ws.bm[(int64_t)(R0 + rl) * g.WW + gword] = x;
+        }
+    }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t tot;
+        const int pre = (int)warp_excl_scan((uint32_t)sm.nrun[lane], tot);
+        sm.rowbase[lane] = pre;
+        if (lane == 31) sm.rowbase[TH] = (int)tot;
+    }
+    __syncthreads();
+    const int R = sm.rowbase[TH];
+    // ---- P1: every run starts as its own root (new label)
+    for (int k = threadIdx.x; k < R; k += NW * 32) sm.p[k] = (uint16_t)k;
+    __syncthreads();
+
+    // ---- P2a: hook -- a run with a foreground pixel among the three above
+    // any of its pixels takes its leftmost upper neighbour as parent (the
+    // decision tree's copy(b)/copy(a)/copy(c)).  Rows are
+    // independent here, so all 32 rows are processed at once.
 #pragma unroll
     for (int i = 0; i < S; i++) {
-        if (i >= nrows) break;
         const int rl = r0 + i;
-        cur = (i == 0) ? 2 : (prev == 0 ? 1 : 0);
-        uint16_t *labc = sm.u.lab[w][cur];
-        const uint16_t *labp = sm.u.lab[w][prev];
-        const uint32_t x = xs[i];
-        const uint32_t xpr = __shfl_up_sync(FULL, x, 1), xnr = __shfl_down_sync(FULL, x, 1);
-        const uint32_t xp = lane == 0 ? 0u : xpr, xn = lane == 31 ? 0u : xnr;
-        const uint32_t hx = x & ~((x << 1) | (xp >> 31));
-
-        // touch pixels: this-row pixels with a foreground pixel among the three above
+        if (rl == 0 || rl >= rows) {
+            sm.mc[rl][lane] = 0u;
+            continue;
+        }
+        const uint32_t x = sm.bm[rl][lane], u = sm.bm[rl - 1][lane];
+        const uint32_t xpr = __shfl_up_sync(FULL, x, 1);
+        const uint32_t upr = __shfl_up_sync(FULL, u, 1), unr = __shfl_down_sync(FULL, u, 1);
+        const uint32_t xp = lane == 0 ? 0u : xpr;
+        const uint32_t up = lane == 0 ? 0u : upr, un = lane == 31 ? 0u : unr;
+        const uint32_t hx = sm.hd[rl][lane];
         const uint32_t t = x & (u | (u << 1) | (up >> 31) | (u >> 1) | (un << 31));
-        // first touch pixel of each run, and the run smear S (for the merge test)
         const uint32_t s = smear_up(t, x);
         const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
         const uint32_t lead = x & ~(x + 1);
-        const uint32_t S = s | (cin ? lead : 0u);
-        const uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
-        // heads of runs with no touch pixel -> new labels
-        uint32_t nh;
-        {
-            const uint32_t sd = smear_down(t, x);
-            const uint32_t cr = carry_in_bwd((x & sd & 1u) != 0, x == FULL) & (x >> 31);
-            const int k = __clz(~x);
-            const uint32_t trail = k == 0 ? 0u : (k == 32 ? FULL : (FULL << (32 - k)));
-            nh = hx & ~(sd | (cr ? trail : 0u));
+        const uint32_t S_ = s | (cin ? lead : 0u);
+        uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
+        sm.mc[rl][lane] = upper_merge_heads(sm.hd[rl - 1][lane], u, up, x, xp, S_);
+        const int lbase = sm.rowbase[rl] + sm.hbase[rl][lane] - 1;
+        while (ft) {
+            const int b = __ffs(ft) - 1;
+            ft &= ft - 1;
+            const int q = 32 * lane + b + leftmost3(u, up, un, b);
+            sm.p[lbase + __popc(hx & upto(b))] = (uint16_t)run_index(sm, rl - 1, q >> 5, q & 31);
         }
-        // one scan for both run ordinals and new-label numbers
-        uint32_t tot;
-        const uint32_t pre = warp_excl_scan(__popc(hx) | (__popc(nh) << 16), tot);
-        const uint32_t base = pre & 0xFFFFu, nbase = pre >> 16;
-        const uint32_t nr = tot & 0xFFFFu, nnew = tot >> 16;
-        sm.hd[w][cur][lane] = hx;
-        sm.bs[w][cur][lane] = base;
-        sm.bm[rl][lane] = x;
-        if (gword < g.WW) ws.bm[(int64_t)(R0 + rl) * g.WW + gword] = x;
-
-        // new labels, numbered in column order = raster order
-        {
-            uint32_t m = nh, k = next + nbase;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                labc[run_ord(hx, base, b)] = (uint16_t)k;
-                sm.p[k] = (uint16_t)k;
-                sm.lpos[k] = (uint16_t)(rl * TW + 32 * lane + b);
-                k++;
-            }
-        }
-        next += nnew;
-        // copy: a touched run takes the label of its leftmost upper neighbour
-        // (the decision tree's copy(b)/copy(a)/copy(c))
-        {
-            uint32_t m = ft;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                const int q = 32 * lane + b + leftmost3(u, up, un, b);
-                const int lq = q >> 5;
-                const int ou = run_ord(sm.hd[w][prev][lq], sm.bs[w][prev][lq], q & 31);
-                labc[run_ord(hx, base, b)] = labp[ou];
-            }
-        }
-        __syncwarp();
-        // merge: the few upper runs whose lower neighbour copied another
-        // label (the decision tree's copy(c,a)/copy(c,d) merges)
-        if (i > 0) {
-            uint32_t m = upper_merge_heads(hu, u, up, x, xp, S);
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                const int q = 32 * lane + b - 1;  // lower pixel h-1 of the run below
-                const int lq = q >> 5;
-                const uint32_t lx = labc[run_ord(sm.hd[w][cur][lq], sm.bs[w][cur][lq], q & 31)];
-                const uint32_t lu = labp[run_ord(hu, bu, b)];
-                if (lx != lu) merge_smem(sm.p, lu, lx);
-            }
-        }
-        // per-row outputs: run labels (for K5) and the border-column labels
-        {
-            uint32_t *dst = reinterpret_cast<uint32_t *>(ws.runlab + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN);
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(labc);
-            for (int k = lane; 2 * k < (int)nr; k += 32) dst[k] = src[k];
-            if (lane == 0) sm.left[rl] = (x & 1u) ? (int16_t)labc[0] : (int16_t)-1;
-            const int lc = vcols - 1;
-            if (lane == (lc >> 5)) sm.right[rl] = ((x >> (lc & 31)) & 1u) ? (int16_t)labc[nr - 1] : (int16_t)-1;
-            if (lane == 0) {
-                if (i == 0) sm.nrow[w][0] = (int)nr;
-                sm.nrow[w][1] = (int)nr;
-            }
-        }
-        __syncwarp();
-        u = x;
-        up = xp;
-        un = xn;
-        hu = hx;
-        bu = base;
-        prev = cur;
-    }
-    if (lane == 0) {
-        sm.used[w] = (int)(next - w * CAPS);
-        sm.last[w] = prev;
     }
     __syncthreads();
-
-    // ---- Phase II: merge across strip boundaries (PARemSP boundary loop,
-    // PAPER.md:971-988, lock-free merger)
-    if (w > 0 && r0 < rows) {
-        const int pw = w - 1, pb = sm.last[pw];
-        const uint32_t uu = sm.bm[r0 - 1][lane], x = sm.bm[r0][lane];
-        const uint16_t *labu = sm.u.lab[pw][pb];
-        const uint16_t *labx = sm.u.lab[w][2];
-        const uint32_t *hdu = sm.hd[pw][pb], *bsu = sm.bs[pw][pb];
-        const uint32_t *hdx = sm.hd[w][2], *bsx = sm.bs[w][2];
-        RowView X = make_row(x);
-        RowView U = make_row(uu);
-        const uint32_t t = x & dilate(U);
-        const uint32_t s = smear_up(t, x);
-        const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
-        const uint32_t lead = x & ~(x + 1);
-        const uint32_t S = s | (cin ? lead : 0u);
-        uint32_t m = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
-        while (m) {  // each lower run with its leftmost upper neighbour
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const int q = 32 * lane + b + leftmost3(uu, U.xp, U.xn, b);
-            const int lq = q >> 5;
-            const uint32_t lu = labu[run_ord(hdu[lq], bsu[lq], q & 31)];
-            const uint32_t lx = labx[run_ord(X.hx, X.base, b)];
-            if (lx != lu) merge_smem(sm.p, lu, lx);
-        }
-        m = upper_merge_heads(U.hx, uu, U.xp, x, X.xp, S);
-        while (m) {  // upper runs whose leftmost lower neighbour has another leftmost upper
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const int q = 32 * lane + b - 1;
-            const int lq = q >> 5;
-            const uint32_t lx = labx[run_ord(hdx[lq], bsx[lq], q & 31)];
-            const uint32_t lu = labu[run_ord(U.hx, U.base, b)];
-            if (lx != lu) merge_smem(sm.p, lu, lx);
-        }
-    }
-    // keep the tile's first and last row labels (the lab buffers are reused below)
-    const int wl = (rows - 1) / S;  // strip holding the tile's last row
+    // ---- P3a: flatten the hooks in increasing index order (Alg. flatten's
+    // "p[i] <- p[p[i]]"): a row's parents lie in the row above,
+    // which is already final, so each row is one parallel step.
     if (w == 0) {
-        const uint16_t *src = sm.u.lab[0][2];
-        for (int k = lane; k < sm.nrow[0][0]; k += 32) sm.toplab[k] = src[k];
-    }
-    if (w == wl) {
-        const uint16_t *src = sm.u.lab[wl][sm.last[wl]];
-        for (int k = lane; k < sm.nrow[wl][1]; k += 32) sm.botlab[k] = src[k];
-    }
-    __syncthreads();
-
-    // ---- Phase III: tile flatten: roots in label order
-    // (= raster order of the creating pixel) get consecutive component
-    // indices.  Warp w walks its own strip's labels in order.
-    const int used_w = sm.used[w];
-    const int lbase = w * CAPS;
-    volatile uint16_t *vp = sm.p;
-    // (a) full path compression
-    for (int i = lane; i < used_w; i += 32) {
-        const int l = lbase + i;
-        uint32_t r = vp[l];
-        while (vp[r] != r) r = vp[r];
-        vp[l] = (uint16_t)r;
-    }
-    __syncthreads();
-    // (b) count roots per strip, then number them in label order
-    int nroot = 0;
-    for (int i0 = 0; i0 < used_w; i0 += 32) {
-        const int i = i0 + lane;
-        nroot += __popc(__ballot_sync(FULL, i < used_w && sm.p[lbase + i] == (uint16_t)(lbase + i)));
-    }
-    if (lane == 0) sm.wscan[w] = nroot;
-    __syncthreads();
-    int coff = 0, ncomp = 0;
-#pragma unroll
-    for (int k = 0; k < NW; k++) {
-        const int v = sm.wscan[k];
-        coff += k < w ? v : 0;
-        ncomp += v;
-    }
-    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
-    for (int i0 = 0; i0 < used_w; i0 += 32) {
-        const int i = i0 + lane;
-        const int l = lbase + i;
-        const bool root = i < used_w && sm.p[l] == (uint16_t)l;
-        const uint32_t bal = __ballot_sync(FULL, root);
-        if (root) {
-            const int c = coff + __popc(bal & ((1u << lane) - 1));
-            const int pos = sm.lpos[l];
-            compkey[c] = (R0 + (pos >> 10)) * g.W + C0 + (pos & (TW - 1));
-            sm.lpos[l] = (uint16_t)c;  // a root's lpos now holds its component
+        volatile uint16_t *vp = sm.p;
+        for (int r = 1; r < rows; r++) {
+            const int b = sm.rowbase[r], e = sm.rowbase[r + 1];
+            for (int k = b + lane; k < e; k += 32) vp[k] = vp[vp[k]];
+            __syncwarp();
         }
-        coff += __popc(bal);
     }
     __syncthreads();
-    // (c) provisional label -> component (for K5); clear the border flags
-    uint16_t *lmap = ws.lmap + (int64_t)tile * CAP;
-    for (int i = lane; i < used_w; i += 32) {
-        const int l = lbase + i;
-        lmap[l] = sm.lpos[sm.p[l]];
+    // ---- P2b: the remaining edges, merged with lock-free Rem's splicing
+    // (the decision tree's copy(c,a)/copy(c,d) merges)
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i;
+        uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const int q = 32 * lane + b - 1;  // lower pixel h-1 of the run below
+            const int a = run_index(sm, rl - 1, lane, b);
+            const int c = run_index(sm, rl, q >> 5, q & 31);
+            merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
+        }
     }
-    for (int c = threadIdx.x; c < ncomp; c += NW * 32) sm.u.cnode[c] = 0;
     __syncthreads();
-    // (d) mark components that touch the tile border
-    auto comp_of = [&](int l) -> int { return sm.lpos[sm.p[l]]; };
-    const int ntop = sm.nrow[0][0], nbot = sm.nrow[wl][1];
-    for (int k = threadIdx.x; k < ntop; k += NW * 32) sm.u.cnode[comp_of(sm.toplab[k])] = 1;
-    for (int k = threadIdx.x; k < nbot; k += NW * 32) sm.u.cnode[comp_of(sm.botlab[k])] = 1;
+    // ---- P3b: final compression (every run -> its root)
+    {
+        volatile uint16_t *vp = sm.p;
+        for (int k = threadIdx.x; k < R; k += NW * 32) {
+            uint32_t r = vp[k];
+            while (vp[r] != r) r = vp[r];
+            vp[k] = (uint16_t)r;
+        }
+    }
+    __syncthreads();
+    // ---- P4a: roots in index order = raster order of first pixels get the
+    // consecutive component numbers (Alg. flatten's k++)
+    const int per = (R + NW * 32 - 1) / (NW * 32);
+    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
+    int cnt = 0;
+    for (int k = k0; k < k1; k++) cnt += sm.p[k] == (uint16_t)k;
+    int ncomp;
+    int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
+    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
+    {
+        int rl = 0;
+        for (int k = k0; k < k1; k++) {
+            if (sm.p[k] != (uint16_t)k) continue;
+            while (sm.rowbase[rl + 1] <= k) rl++;
+            // the head of the (k - rowbase)-th run of row rl
+            const int o = k - sm.rowbase[rl];
+            int lw = 0;
+            while (lw < WPR - 1 && sm.hbase[rl][lw + 1] <= o) lw++;
+            uint32_t hm = sm.hd[rl][lw];
+            for (int j = o - sm.hbase[rl][lw]; j > 0; j--) hm &= hm - 1;  // drop earlier heads
+            const int col = 32 * lw + __ffs(hm) - 1;
+            compkey[cidx] = (R0 + rl) * g.W + C0 + col;
+            sm.p[k] = (uint16_t)(0x8000 | cidx);  // root: flag | component
+            cidx++;
+        }
+    }
+    __syncthreads();
+    auto comp_of = [&](int k) -> int {
+        const uint32_t pk = sm.p[k];
+        return (int)((pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu));
+    };
+    auto root_of = [&](int k) -> int {
+        const uint32_t pk = sm.p[k];
+        return (pk & 0x8000u) ? k : (int)pk;
+    };
+    // ---- P4b: mark components that touch the tile border (flag 0x4000 on the root)
+    auto mark = [&](int k) {
+        const int r = root_of(k);
+        atomicOr(reinterpret_cast<unsigned int *>(sm.p) + (r >> 1), 0x4000u << (16 * (r & 1)));
+    };
+    const int lc = vcols - 1;
+    for (int k = threadIdx.x; k < sm.rowbase[1]; k += NW * 32) mark(k);
+    for (int k = sm.rowbase[rows - 1] + threadIdx.x; k < sm.rowbase[rows]; k += NW * 32) mark(k);
     for (int r = threadIdx.x; r < rows; r += NW * 32) {
-        if (sm.left[r] >= 0) sm.u.cnode[comp_of(sm.left[r])] = 1;
-        if (sm.right[r] >= 0) sm.u.cnode[comp_of(sm.right[r])] = 1;
+        if (sm.bm[r][0] & 1u) mark(sm.rowbase[r]);
+        if ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) mark(sm.rowbase[r + 1] - 1);
     }
     __syncthreads();
-    // (e) border components -> global union-find nodes
-    const int cper = (ncomp + NW * 32 - 1) / (NW * 32);
-    const int c0 = threadIdx.x * cper, c1 = min(ncomp, c0 + cper);
+    // ---- P4c: border components -> global union-find nodes
     int bc = 0;
-    for (int c = c0; c < c1; c++) bc += sm.u.cnode[c] != 0;
+    for (int k = k0; k < k1; k++) bc += (sm.p[k] & 0xC000u) == 0xC000u;
     int nborder;
     int bidx = block_excl_scan(bc, sm.wscan, nborder);
     int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
     const int nodebase = tile * CAPB;
-    for (int c = c0; c < c1; c++) {
-        if (sm.u.cnode[c]) {
-            const int node = nodebase + bidx;
+    for (int k = k0; k < k1; k++) {
+        const uint32_t pk = sm.p[k];
+        if (!(pk & 0x8000u)) continue;
+        const int c = (int)(pk & 0x3FFFu);
+        if (pk & 0x4000u) {
+            const int node = nodebase + bidx++;
             compnode[c] = node;
             ws.gparent[node] = node;
             ws.gkey[node] = compkey[c];
-            sm.u.cnode[c] = (uint16_t)(bidx + 1);
-            bidx++;
         } else {
             compnode[c] = -1;
         }
     }
     __syncthreads();
-    // (f) nodes of the border pixels, for K2
-    auto node_of = [&](int l) -> int { return nodebase + (int)sm.u.cnode[comp_of(l)] - 1; };
-    for (int k = threadIdx.x; k < ntop; k += NW * 32) ws.topnode[tile * MAXRUN + k] = node_of(sm.toplab[k]);
-    for (int k = threadIdx.x; k < nbot; k += NW * 32) ws.botnode[tile * MAXRUN + k] = node_of(sm.botlab[k]);
-    for (int r = threadIdx.x; r < rows; r += NW * 32) {
-        const int64_t o = (int64_t)tx * g.H + R0 + r;
-        ws.leftnode[o] = sm.left[r] >= 0 ? node_of(sm.left[r]) : -1;
-        ws.rightnode[o] = sm.right[r] >= 0 ? node_of(sm.right[r]) : -1;
+    // ---- P4d: outputs -- component of every run (for K5) and the nodes of the
+    // border pixels (for K2)
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i;
+        if (rl >= rows) break;
+        const int b = sm.rowbase[rl], n = sm.nrun[rl];
+        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
+        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(b + o);
+    }
+    {
+        const int ntop = sm.nrun[0], bb = sm.rowbase[rows - 1], nbot = sm.nrun[rows - 1];
+        for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[tile * MAXRUN + o] = compnode[comp_of(o)];
+        for (int o = threadIdx.x; o < nbot; o += NW * 32) ws.botnode[tile * MAXRUN + o] = compnode[comp_of(bb + o)];
+        for (int r = threadIdx.x; r < rows; r += NW * 32) {
+            const int64_t off = (int64_t)tx * g.H + R0 + r;
+            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? compnode[comp_of(sm.rowbase[r])] : -1;
+            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? compnode[comp_of(sm.rowbase[r + 1] - 1)] : -1;
+        }
     }
     if (threadIdx.x == 0) {
         int32_t *meta = ws.meta + (int64_t)tile * META;
@@ -571,7 +501,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         meta[META_NBORDER] = nborder;
         meta[META_ROWS] = rows;
     }
-    if (lane == 0) ws.meta[(int64_t)tile * META + META_USED + w] = used_w;
 }
 
 // ========================================================================= K2
@@ -636,70 +565,73 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
 }
 
 // ========================================================================= K3
-// Per tile: component c is a global root iff it lies inside the tile or its
-// node is a root of the global forest (its key is the component's minimum,
-// i.e. its first pixel in raster order).  Counts roots per row and gives
-// each root its rank inside its (row, tile-column) segment.
-__global__ void __launch_bounds__(256)
+// One warp per tile: component c is a global root iff it lies inside the
+// tile or its node is a root of the global forest (its key is the
+// component's minimum, i.e. its first pixel in raster order).  Counts roots
+// per (row, tile-column) segment and ranks each root inside its segment.
+constexpr int K3_WARPS = 8;
+__global__ void __launch_bounds__(K3_WARPS * 32)
 k_roots(Geometry g, Workspace ws) {
-    __shared__ int cntrow[TH], rowbase[TH], wscan[8];
-    const int tile = blockIdx.x;
-    const int tx = tile % g.nTx, ty = tile / g.nTx, R0 = ty * TH;
-    if (tile == 0) {  // reset the scan's lookback state for K4
+    __shared__ int cnt[K3_WARPS][TH + 1];
+    const int lane = lane_id(), wi = threadIdx.x >> 5;
+    const int tile = blockIdx.x * K3_WARPS + wi;
+    if (blockIdx.x == 0) {  // reset the scan's lookback state for K4
         for (int i = threadIdx.x; i < g.nscan; i += blockDim.x) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
     }
+    if (tile >= g.nT) return;
+    const int tx = tile % g.nTx, ty = tile / g.nTx, R0 = ty * TH;
     const int32_t *meta = ws.meta + (int64_t)tile * META;
     const int ncomp = meta[META_NCOMP], rows = meta[META_ROWS];
-    if (threadIdx.x < TH) cntrow[threadIdx.x] = 0;
     const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
     const int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
     uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
-    const int per = (ncomp + 255) / 256;
-    const int c0 = threadIdx.x * per, c1 = min(ncomp, c0 + per);
-    int cnt = 0;
-    for (int c = c0; c < c1; c++) {
-        int node = compnode[c];
-        cnt += node < 0 || __ldcg(ws.gparent + node) == node;
-    }
-    __syncthreads();
-    // block scan over 8 warps
-    uint32_t tot;
-    int pre = (int)warp_excl_scan((uint32_t)cnt, tot);
-    if (lane_id() == 0) wscan[threadIdx.x >> 5] = (int)tot;
-    __syncthreads();
-    int off = 0;
-    for (int i = 0; i < (int)(threadIdx.x >> 5); i++) off += wscan[i];
-    int rank = pre + off;
-    // per-row counts
-    for (int c = c0; c < c1; c++) {
-        int node = compnode[c];
-        bool root = node < 0 || __ldcg(ws.gparent + node) == node;
-        if (root) atomicAdd(&cntrow[compkey[c] / g.W - R0], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int r = 0; r < TH; r++) { rowbase[r] = s; s += cntrow[r]; }
-    }
-    __syncthreads();
-    for (int c = c0; c < c1; c++) {
-        int node = compnode[c];
-        bool root = node < 0 || __ldcg(ws.gparent + node) == node;
-        if (root) {
-            int rl = compkey[c] / g.W - R0;
-            int rk = rank - rowbase[rl];
-            comprank[c] = ((uint32_t)rl << 16) | (uint32_t)rk;
-            if (node >= 0) {
-                ws.gnodeseg[node] = (R0 + rl) * g.nTx + tx;
-                ws.gnoderank[node] = rk;
-            }
-            rank++;
-        } else {
-            comprank[c] = 0xFFFFFFFFu;
+    int *c_row = cnt[wi];
+    c_row[lane] = 0;
+    if (lane == 0) c_row[TH] = 0;
+    __syncwarp();
+    // pass 1: roots per row
+    for (int c0 = 0; c0 < ncomp; c0 += 32) {
+        const int c = c0 + lane;
+        if (c < ncomp) {
+            const int node = compnode[c];
+            if (node < 0 || __ldcg(ws.gparent + node) == node) atomicAdd(&c_row[compkey[c] / g.W - R0], 1);
         }
     }
-    if (threadIdx.x < rows) ws.segcnt[(int64_t)(R0 + threadIdx.x) * g.nTx + tx] = cntrow[threadIdx.x];
+    __syncwarp();
+    uint32_t tot;
+    const int rowstart = (int)warp_excl_scan((uint32_t)c_row[lane], tot);
+    const int mycnt = c_row[lane];
+    __syncwarp();
+    c_row[lane] = rowstart;
+    __syncwarp();
+    if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = mycnt;
+    // pass 2: rank = (roots before it in the tile) - (roots in earlier rows)
+    int run = 0;
+    for (int c0 = 0; c0 < ncomp; c0 += 32) {
+        const int c = c0 + lane;
+        bool root = false;
+        int node = -1, rl = 0;
+        if (c < ncomp) {
+            node = compnode[c];
+            root = node < 0 || __ldcg(ws.gparent + node) == node;
+            rl = compkey[c] / g.W - R0;
+        }
+        const uint32_t bal = __ballot_sync(FULL, root);
+        if (c < ncomp) {
+            if (root) {
+                const int rk = run + __popc(bal & ((1u << lane) - 1)) - c_row[rl];
+                comprank[c] = ((uint32_t)rl << 16) | (uint32_t)rk;
+                if (node >= 0) {
+                    ws.gnodeseg[node] = (R0 + rl) * g.nTx + tx;
+                    ws.gnoderank[node] = rk;
+                }
+            } else {
+                comprank[c] = 0xFFFFFFFFu;
+            }
+        }
+        run += __popc(bal);
+    }
 }
 
 // ========================================================================= K4
@@ -766,117 +698,120 @@ k_scan(Geometry g, Workspace ws, int32_t *n_components) {
     }
 }
 
-// ========================================================================= K5
-struct K5Smem {
-    int32_t flab[CAP];           // provisional label -> final label
-    int32_t rowbuf[NW][TW];      // per-warp row staging (run labels, then the swizzled output row)
-};
-
-// Final label of a tile component (flatten's consecutive numbering,
-// PAPER.md:714-715, in raster order): roots from their segment offset and
-// rank; border components that are not roots from their global root's.
-__device__ __forceinline__ int32_t comp_label(const Geometry &g, const Workspace &ws, int tile,
-                                              int R0, int tx, int c) {
-    const uint32_t cr = ws.comprank[(int64_t)tile * CAPC + c];
-    if (cr != 0xFFFFFFFFu)
-        return ws.segoff[(int64_t)(R0 + (int)(cr >> 16)) * g.nTx + tx] + (int)(cr & 0xFFFF) + 1;
-    const int root = gfind_ro(ws.gparent, ws.compnode[(int64_t)tile * CAPC + c]);
-    return ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+// ======================================================================== K4b
+// One warp per tile: the final label of every tile component, i.e.
+// flatten's consecutive numbering in raster order: a root
+// gets its segment's offset + its rank + 1; a border component that is not a
+// root gets its global root's label.
+__global__ void __launch_bounds__(256)
+k_final(Geometry g, Workspace ws) {
+    const int lane = lane_id();
+    const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (tile >= g.nT) return;
+    const int tx = tile % g.nTx, R0 = (tile / g.nTx) * TH;
+    const int ncomp = ws.meta[(int64_t)tile * META + META_NCOMP];
+    const uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
+    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
+    int32_t *complab = ws.complab + (int64_t)tile * CAPC;
+    for (int c0 = 0; c0 < ncomp; c0 += 64) {
+        // two components per lane in flight
+        const int ca = c0 + lane, cb = c0 + 32 + lane;
+        const uint32_t ra = ca < ncomp ? comprank[ca] : 0u, rb = cb < ncomp ? comprank[cb] : 0u;
+        int la = 0, lb = 0;
+        if (ca < ncomp) {
+            if (ra != 0xFFFFFFFFu) {
+                la = ws.segoff[(int64_t)(R0 + (int)(ra >> 16)) * g.nTx + tx] + (int)(ra & 0xFFFF) + 1;
+            } else {
+                const int root = gfind_ro(ws.gparent, compnode[ca]);
+                la = ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+            }
+        }
+        if (cb < ncomp) {
+            if (rb != 0xFFFFFFFFu) {
+                lb = ws.segoff[(int64_t)(R0 + (int)(rb >> 16)) * g.nTx + tx] + (int)(rb & 0xFFFF) + 1;
+            } else {
+                const int root = gfind_ro(ws.gparent, compnode[cb]);
+                lb = ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+            }
+        }
+        if (ca < ncomp) complab[ca] = la;
+        if (cb < ncomp) complab[cb] = lb;
+    }
 }
 
-__global__ void __launch_bounds__(NW * 32, 3)
+// ========================================================================= K5
+// Labeling phase: one warp per 1024-px row segment.  Lane
+// j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
+// warp is one contiguous 512-byte stretch of the output row.
+constexpr int K5_WARPS = 8;
+__global__ void __launch_bounds__(K5_WARPS * 32)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    K5Smem &sm = *reinterpret_cast<K5Smem *>(smem_raw);
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
-    const int tx = tile % g.nTx, ty = tile / g.nTx;
-    const int R0 = ty * TH, C0 = tx * TW;
-    const int32_t *meta = ws.meta + (int64_t)tile * META;
-    const int rows = meta[META_ROWS];
+    __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
+    const int lane = lane_id(), wi = threadIdx.x >> 5;
+    const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
+    if (seg >= g.nseg) return;
+    const int row = (int)(seg / g.nTx), tx = (int)(seg % g.nTx);
+    const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
-
-    // this warp's rows are w, w+NW, ...; the next row's mask is always in flight
-    auto load_mask = [&](int rl) -> uint32_t {
-        return (rl < rows && gword < g.WW) ? __ldcs(ws.bm + (int64_t)(R0 + rl) * g.WW + gword) : 0u;
-    };
-    uint32_t xnext = load_mask(w);
-    // provisional label -> final label (warp w: strip w's labels)
+    const uint32_t x = gword < g.WW ? __ldcs(ws.bm + (int64_t)row * g.WW + gword) : 0u;
+    const uint32_t xl = __shfl_up_sync(FULL, x, 1);
+    const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
+    uint32_t nr;
+    const uint32_t base = warp_excl_scan(__popc(hx), nr);
+    int32_t *rowlab = s_lab[wi];
     {
-        const int used = meta[META_USED + w];
-        const uint16_t *lmap = ws.lmap + (int64_t)tile * CAP + w * CAPS;
-        for (int i = lane; i < used; i += 32)
-            sm.flab[w * CAPS + i] = comp_label(g, ws, tile, R0, tx, lmap[i]);
+        const uint16_t *rc = ws.runcomp + seg * MAXRUN;
+        const int32_t *complab = ws.complab + (int64_t)tile * CAPC;
+        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)];
     }
-    __syncthreads();
-
-    int32_t *buf = sm.rowbuf[w];
-    int32_t *rowlab = buf + MAXRUN;  // upper half: run labels of the current row
-#pragma unroll 1
-    for (int i = 0; i < TH / NW; i++) {
-        const int rl = w + i * NW;
-        if (rl >= rows) break;
-        const int row = R0 + rl;
-        const uint32_t x = xnext;
-        xnext = load_mask(rl + NW);
-        const uint32_t xl = __shfl_up_sync(FULL, x, 1);
-        const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
-        uint32_t nr;
-        const uint32_t base = warp_excl_scan(__popc(hx), nr);
-        const uint16_t *rlab = ws.runlab + ((int64_t)row * g.nTx + tx) * MAXRUN;
-        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = sm.flab[__ldcs(rlab + k)];
-        __syncwarp();
-        // walk this lane's 32 pixels: the label changes only at run heads
-        int v[32];
-        {
-            int ord = (int)base;
-            int cur = ((x & 1u) && !(hx & 1u)) ? rowlab[ord - 1] : 0;
+    __syncwarp();
+    int32_t *out = labels + (int64_t)row * g.W + C0;
 #pragma unroll
-            for (int b = 0; b < 32; b++) {
-                if ((hx >> b) & 1u) cur = rowlab[ord++];
-                v[b] = ((x >> b) & 1u) ? cur : 0;
-            }
+    for (int c = 0; c < 8; c++) {
+        const int wsrc = 4 * c + (lane >> 3);  // lane-word holding these 4 pixels
+        const int b0 = 4 * (lane & 7);
+        const uint32_t xw = __shfl_sync(FULL, x, wsrc);
+        const uint32_t hw = __shfl_sync(FULL, hx, wsrc);
+        const uint32_t bw = __shfl_sync(FULL, base, wsrc);
+        const uint32_t nib = (xw >> b0) & 0xFu, hn = (hw >> b0) & 0xFu;
+        int ord = (int)bw + __popc(hw & upto(b0)) - 1;  // run containing (or before) pixel b0
+        int L = ord >= 0 ? rowlab[ord] : 0;
+        int v0 = (nib & 1u) ? L : 0;
+        if (hn & 2u) L = rowlab[++ord];
+        int v1 = (nib & 2u) ? L : 0;
+        if (hn & 4u) L = rowlab[++ord];
+        int v2 = (nib & 4u) ? L : 0;
+        if (hn & 8u) L = rowlab[++ord];
+        int v3 = (nib & 8u) ? L : 0;
+        const int P = 128 * c + 4 * lane;
+        if (g.aligned) {
+            if (P < vcols) __stcs(reinterpret_cast<int4 *>(out + P), make_int4(v0, v1, v2, v3));
+        } else {
+            if (P < vcols) __stcs(out + P, v0);
+            if (P + 1 < vcols) __stcs(out + P + 1, v1);
+            if (P + 2 < vcols) __stcs(out + P + 2, v2);
+            if (P + 3 < vcols) __stcs(out + P + 3, v3);
         }
-        __syncwarp();
-        // stage the row: lane's 32 labels = 8 16-byte chunks, XOR-swizzled so
-        // both the row-wise writes and the coalesced reads are conflict-free
-#pragma unroll
-        for (int j = 0; j < 8; j++)
-            *reinterpret_cast<int4 *>(buf + lane * 32 + ((j ^ (lane & 7)) << 2)) =
-                make_int4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        __syncwarp();
-        int32_t *out = labels + (int64_t)row * g.W + C0;
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            const int P = 128 * c + 4 * lane;          // first pixel of this lane's chunk
-            const int jw = P >> 5, jj = (P >> 2) & 7;  // source lane-word and chunk
-            const int4 o = *reinterpret_cast<const int4 *>(buf + jw * 32 + ((jj ^ (jw & 7)) << 2));
-            if (g.aligned) {
-                if (P < vcols) __stcs(reinterpret_cast<int4 *>(out + P), o);
-            } else {
-                if (P < vcols) __stcs(out + P, o.x);
-                if (P + 1 < vcols) __stcs(out + P + 1, o.y);
-                if (P + 2 < vcols) __stcs(out + P + 2, o.z);
-                if (P + 3 < vcols) __stcs(out + P + 3, o.w);
-            }
-        }
-        __syncwarp();
     }
 }
 
 // ==================================================================== host
 static bool g_attr_done = false;
 
+int pipeline_launches(const Geometry &g) {
+    const int nh = (g.nTy - 1) * g.nTx;
+    const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
+    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+}
+
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev) {
     cudaError_t e;
-    const int k1smem = (int)sizeof(K1Smem), k5smem = (int)sizeof(K5Smem);
+    const int k1smem = (int)sizeof(K1Smem);
     if (!g_attr_done) {
         e = cudaFuncSetAttribute(k_tile_local, cudaFuncAttributeMaxDynamicSharedMemorySize, k1smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_write, cudaFuncAttributeMaxDynamicSharedMemorySize, k5smem);
         if (e != cudaSuccess) return e;
         g_attr_done = true;
     }
@@ -891,11 +826,13 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
     const int64_t warps = nh + (nv + 31) / 32;
     if (warps > 0) k_border<<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(g, ws, nh);
     mark(K_ROOTS);
-    k_roots<<<g.nT, 256, 0, stream>>>(g, ws);
+    k_roots<<<(g.nT + K3_WARPS - 1) / K3_WARPS, K3_WARPS * 32, 0, stream>>>(g, ws);
     mark(K_SCAN);
     k_scan<<<g.nscan, SCAN_THREADS, 0, stream>>>(g, ws, n_components);
+    mark(K_FINAL);
+    k_final<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws);
     mark(K_WRITE);
-    k_write<<<g.nT, NW * 32, k5smem, stream>>>(g, ws, labels);
+    k_write<<<(unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream>>>(g, ws, labels);
     mark(K_COUNT);
     return cudaGetLastError();
 }

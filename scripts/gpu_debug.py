@@ -7,7 +7,7 @@ import paper_1606_05973_b200 as ccl
 L = ccl._L
 L.ccl_debug_workspace.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
 cudart = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
-names = ["bm","runlab","lmap","compkey","compnode","comprank","gparent","gkey","gnodeseg","gnoderank","top","bot","left","right","meta","segcnt","segoff","scanstate","ticket"]
+names = ["bm","runcomp","compkey","compnode","comprank","complab","gparent","gkey","gnodeseg","gnoderank","top","bot","left","right","meta","segcnt","segoff","scanstate","ticket"]
 def dump(plan, name, dtype, count):
     base = ctypes.c_void_p(); offs = (ctypes.c_uint64 * 32)()
     n = L.ccl_debug_workspace(plan._p, ctypes.byref(base), offs, 32)
@@ -28,10 +28,10 @@ print("gpu N", int(n.item())); print(lab.cpu().numpy())
 lo, no = oracle.label(img); print("oracle N", no); print(lo)
 WW = (W + 31)//32; nTx = (W+1023)//1024; nTy = (H+31)//32
 print("bm", [hex(v) for v in dump(plan, "bm", np.uint32, H*WW)])
-rl = dump(plan, "runlab", np.uint16, H*nTx*512).reshape(H, nTx, 512)
-for r in range(H): print("runlab row", r, rl[r,0,:8])
-meta = dump(plan, "meta", np.int32, nTx*nTy*16).reshape(-1,16); print("meta", meta)
-lm = dump(plan, "lmap", np.uint16, 8192); print("lmap[0:8]", lm[:8], "lmap[1024:1032]", lm[1024:1032])
+rl = dump(plan, "runcomp", np.uint16, H*nTx*512).reshape(H, nTx, 512)
+for r in range(H): print("runcomp row", r, rl[r,0,:8])
+meta = dump(plan, "meta", np.int32, nTx*nTy*4).reshape(-1,4); print("meta", meta)
+print("complab", dump(plan, "complab", np.int32, 16))
 print("compkey", dump(plan, "compkey", np.int32, 16)); print("compnode", dump(plan, "compnode", np.int32, 16))
 print("comprank", [hex(v) for v in dump(plan, "comprank", np.uint32, 16)])
 print("segcnt", dump(plan, "segcnt", np.int32, H*nTx)); print("segoff", dump(plan, "segoff", np.int32, H*nTx))

@@ -130,10 +130,10 @@ def test_label_host_end_to_end():
 def test_kernel_times_profiling():
     img = torch.from_numpy(synth.bernoulli(640, 2048, 0.5, 3)).cuda()
     plan = ccl.Plan(640, 2048)
-    plan.set_profiling(True)
+    plan.set_profiling(1)
     plan.label(img)
     t = plan.kernel_times()
-    assert set(t) == {"k_tile_local", "k_border", "k_roots", "k_scan", "k_write"}
+    assert set(t) == {"k_tile_local", "k_border", "k_roots", "k_scan", "k_final", "k_write"}
     assert all(v >= 0 for v in t.values())
 
 
