@@ -414,24 +414,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     for (int k = k0; k < k1; k++) cnt += sm.p[k] == (uint16_t)k;
     int ncomp;
     int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
-    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
-    {
-        int rl = 0;
-        for (int k = k0; k < k1; k++) {
-            if (sm.p[k] != (uint16_t)k) continue;
-            while (sm.rowbase[rl + 1] <= k) rl++;
-            // the head of the (k - rowbase)-th run of row rl
-            const int o = k - sm.rowbase[rl];
-            int lw = 0;
-            while (lw < WPR - 1 && sm.hbase[rl][lw + 1] <= o) lw++;
-            uint32_t hm = sm.hd[rl][lw];
-            for (int j = o - sm.hbase[rl][lw]; j > 0; j--) hm &= hm - 1;  // drop earlier heads
-            const int col = 32 * lw + __ffs(hm) - 1;
-            compkey[cidx] = (R0 + rl) * g.W + C0 + col;
-            sm.p[k] = (uint16_t)(0x8000 | cidx);  // root: flag | component
-            cidx++;
-        }
-    }
+    for (int k = k0; k < k1; k++)
+        if (sm.p[k] == (uint16_t)k) sm.p[k] = (uint16_t)(0x8000 | cidx++);  // root: flag | component
     __syncthreads();
     auto comp_of = [&](int k) -> int {
         const uint32_t pk = sm.p[k];
@@ -441,7 +425,23 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         const uint32_t pk = sm.p[k];
         return (pk & 0x8000u) ? k : (int)pk;
     };
-    // ---- P4b: mark components that touch the tile border (flag 0x4000 on the root)
+    // ---- P4b: key of each component = raster index of its root run's head
+    // (its first pixel); mark components that touch the tile border (flag
+    // 0x4000 on the root)
+    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i;
+        if (rl >= rows) break;
+        uint32_t hm = sm.hd[rl][lane];
+        int k = sm.rowbase[rl] + sm.hbase[rl][lane];
+        while (hm) {
+            const int b = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const uint32_t pk = sm.p[k++];
+            if (pk & 0x8000u) compkey[pk & 0x3FFFu] = (R0 + rl) * g.W + C0 + 32 * lane + b;
+        }
+    }
     auto mark = [&](int k) {
         const int r = root_of(k);
         atomicOr(reinterpret_cast<unsigned int *>(sm.p) + (r >> 1), 0x4000u << (16 * (r & 1)));
