@@ -288,3 +288,10 @@ extern "C" int ccl_debug_workspace(ccl_plan p, void **base, uint64_t *offs, int 
     for (int i = 0; i < A_COUNT && i < cap; i++) offs[i] = o[i];
     return A_COUNT;
 }
+
+namespace cclb { extern int g_k1_stop, g_k1_exper; }
+extern "C" int ccl_debug_set(int key, int value) {
+    if (key == 1) { cclb::g_k1_stop = value; return 0; }
+    if (key == 2) { cclb::g_k1_exper = value; return 0; }
+    return 1;
+}

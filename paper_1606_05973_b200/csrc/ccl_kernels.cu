@@ -4,9 +4,9 @@
 //   K1 k_tile_local   one CTA per 32x1024 tile.  128-bit streaming loads of the
 //                     image, packed into 32-bit row masks; the runs of the tile
 //                     are its provisional labels (index order = raster order).
-//                     Scan: every run hooks to its leftmost upper neighbour
-//                     (Scan_ARemSP's copy), all rows at once;
-//                     flatten of the hooks in increasing order;
+//                     Scan: every run copies its leftmost upper neighbour's
+//                     label (Scan_ARemSP's copy), 8 strips
+//                     at once; a short find resolves the copies;
 //                     the few remaining edges merged with a lock-free Rem's
 //                     union with splicing (merge / merger, PAPER.md:669-698,
 //                     1001-1046); roots numbered in raster order.
@@ -284,12 +284,24 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
     return hu & x1 & (s2 | u2);
 }
 
+// A merge candidate at upper head h is also redundant when the gap before
+// h is a single pixel (upper pixel h-2 is foreground) and the row above the
+// upper row has a foreground pixel at h-1: both upper runs touch that pixel,
+// so the lower run is joined to h's run through edges that are processed
+// anyway (the row pair above, and the edge at h-2 to the left).  Candidates
+// bridged this way are the bulk of them on images with isolated holes.
+__device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32_t d) {
+    const uint32_t dpr = __shfl_up_sync(FULL, d, 1);
+    const uint32_t dp = lane_id() == 0 ? 0u : dpr;
+    return ((u << 2) | (up >> 30)) & ((d << 1) | (dp >> 31));
+}
+
 __device__ __forceinline__ int run_index(const K1Smem &sm, int r, int lane_word, int bit) {
     return sm.rowbase[r] + sm.hbase[r][lane_word] + __popc(sm.hd[r][lane_word] & upto(bit)) - 1;
 }
 
 __global__ void __launch_bounds__(NW * 32, 4)
-k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
+k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop, int exper) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
 
@@ -301,6 +313,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;  // this lane's word index in the image row
     const int r0 = w * S;
+    volatile uint16_t *vp = sm.p;
 
     // ---- P0: image -> row masks, run heads, per-word run counts
     {
@@ -331,19 +344,27 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
     }
     __syncthreads();
     const int R = sm.rowbase[TH];
-    // ---- P1: every run starts as its own root (new label)
-    for (int k = threadIdx.x; k < R; k += NW * 32) sm.p[k] = (uint16_t)k;
-    __syncthreads();
 
-    // ---- P2a: hook -- a run with a foreground pixel among the three above
-    // any of its pixels takes its leftmost upper neighbour as parent (the
-    // decision tree's copy(b)/copy(a)/copy(c)).  Rows are
-    // independent here, so all 32 rows are processed at once.
+    if (stop <= 0) return;
+    // ---- P2a: scan.  Every run starts as a new label; a
+    // run with a foreground pixel among the three above any of its pixels
+    // instead copies its leftmost upper neighbour's label (the decision
+    // tree's copy(b)/copy(a)/copy(c)).  Each warp walks its
+    // own rows in order, so inside a strip a run copies its upper neighbour's
+    // parent (already final within the strip); a strip's first row copies the
+    // raw run index of the strip above.
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
-        if (rl == 0 || rl >= rows) {
+        if (rl >= rows) {
             sm.mc[rl][lane] = 0u;
+            continue;
+        }
+        const int rb = sm.rowbase[rl], re = sm.rowbase[rl + 1];
+        for (int k = rb + lane; k < re; k += 32) vp[k] = (uint16_t)k;
+        if (rl == 0) {
+            sm.mc[rl][lane] = 0u;
+            __syncwarp();
             continue;
         }
         const uint32_t x = sm.bm[rl][lane], u = sm.bm[rl - 1][lane];
@@ -358,60 +379,64 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         const uint32_t lead = x & ~(x + 1);
         const uint32_t S_ = s | (cin ? lead : 0u);
         uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
-        sm.mc[rl][lane] = upper_merge_heads(sm.hd[rl - 1][lane], u, up, x, xp, S_);
-        const int lbase = sm.rowbase[rl] + sm.hbase[rl][lane] - 1;
+        uint32_t mc = upper_merge_heads(sm.hd[rl - 1][lane], u, up, x, xp, S_);
+        if (rl >= 2) mc &= ~hole_bridged(u, up, sm.bm[rl - 2][lane]);
+        sm.mc[rl][lane] = mc;
+        const int lbase = rb + sm.hbase[rl][lane] - 1;
+        const bool instrip = i > 0;
+        __syncwarp();
         while (ft) {
             const int b = __ffs(ft) - 1;
             ft &= ft - 1;
             const int q = 32 * lane + b + leftmost3(u, up, un, b);
-            sm.p[lbase + __popc(hx & upto(b))] = (uint16_t)run_index(sm, rl - 1, q >> 5, q & 31);
+            const int ui = run_index(sm, rl - 1, q >> 5, q & 31);
+            vp[lbase + __popc(hx & upto(b))] = instrip ? vp[ui] : (uint16_t)ui;
         }
+        __syncwarp();
     }
     __syncthreads();
-    // ---- P3a: flatten the hooks in increasing index order (Alg. flatten's
-    // "p[i] <- p[p[i]]"): a row's parents lie in the row above,
-    // which is already final, so each row is one parallel step.
-    if (w == 0) {
-        volatile uint16_t *vp = sm.p;
-        for (int r = 1; r < rows; r++) {
-            const int b = sm.rowbase[r], e = sm.rowbase[r + 1];
-            for (int k = b + lane; k < e; k += 32) vp[k] = vp[vp[k]];
-            __syncwarp();
-        }
+    if (stop <= 1) return;
+    // ---- P3a: resolve the hooks: a chain crosses at most one run per strip
+    // above, so a find per run is short; runs point at their roots afterwards
+    // (Alg. flatten's p[i] <- p[p[i]]).
+    const int per = (R + NW * 32 - 1) / (NW * 32);
+    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
+    for (int k = k0; k < k1; k++) {
+        uint32_t r = vp[k];
+        while (vp[r] != r) r = vp[r];
+        vp[k] = (uint16_t)r;
     }
     __syncthreads();
+    if (stop <= 2) return;
     // ---- P2b: the remaining edges, merged with lock-free Rem's splicing
-    // (the decision tree's copy(c,a)/copy(c,d) merges)
+    // (the decision tree's copy(c,a)/copy(c,d) merges);
+    // most candidates already share a root.
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
+        if (exper == 2) m = 0;
         while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
             const int q = 32 * lane + b - 1;  // lower pixel h-1 of the run below
             const int a = run_index(sm, rl - 1, lane, b);
             const int c = run_index(sm, rl, q >> 5, q & 31);
-            merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
+            if (vp[a] != vp[c] && exper != 1) merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
         }
     }
     __syncthreads();
-    // ---- P3b: final compression (every run -> its root)
-    {
-        volatile uint16_t *vp = sm.p;
-        for (int k = threadIdx.x; k < R; k += NW * 32) {
-            uint32_t r = vp[k];
-            while (vp[r] != r) r = vp[r];
-            vp[k] = (uint16_t)r;
-        }
-    }
-    __syncthreads();
-    // ---- P4a: roots in index order = raster order of first pixels get the
-    // consecutive component numbers (Alg. flatten's k++)
-    const int per = (R + NW * 32 - 1) / (NW * 32);
-    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
+    if (stop <= 3) return;
+    // ---- P3b/P4a: final compression; roots in index order = raster order of
+    // first pixels get the consecutive component numbers (Alg. flatten's k++,
+    // PAPER.md:714-715)
     int cnt = 0;
-    for (int k = k0; k < k1; k++) cnt += sm.p[k] == (uint16_t)k;
+    for (int k = k0; k < k1; k++) {
+        uint32_t r = vp[k];
+        while (vp[r] != r) r = vp[r];
+        vp[k] = (uint16_t)r;
+        cnt += r == (uint32_t)k;
+    }
     int ncomp;
     int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
     for (int k = k0; k < k1; k++)
@@ -425,21 +450,26 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         const uint32_t pk = sm.p[k];
         return (pk & 0x8000u) ? k : (int)pk;
     };
-    // ---- P4b: key of each component = raster index of its root run's head
-    // (its first pixel); mark components that touch the tile border (flag
-    // 0x4000 on the root)
+    if (stop <= 4) return;
+    // ---- P4b: per run head: its component (output for K5), and for root
+    // runs the component key = raster index of the head (the first pixel);
+    // mark components that touch the tile border (flag 0x4000 on the root)
     int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         if (rl >= rows) break;
         uint32_t hm = sm.hd[rl][lane];
-        int k = sm.rowbase[rl] + sm.hbase[rl][lane];
+        int o = sm.hbase[rl][lane];
+        const int rb = sm.rowbase[rl];
+        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
         while (hm) {
             const int b = __ffs(hm) - 1;
             hm &= hm - 1;
-            const uint32_t pk = sm.p[k++];
-            if (pk & 0x8000u) compkey[pk & 0x3FFFu] = (R0 + rl) * g.W + C0 + 32 * lane + b;
+            const uint32_t pk = sm.p[rb + o];
+            const uint32_t c = (pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu);
+            dst[o++] = (uint16_t)c;
+            if (pk & 0x8000u) compkey[c] = (R0 + rl) * g.W + C0 + 32 * lane + b;
         }
     }
     auto mark = [&](int k) {
@@ -454,6 +484,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         if ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) mark(sm.rowbase[r + 1] - 1);
     }
     __syncthreads();
+    if (stop <= 5) return;
     // ---- P4c: border components -> global union-find nodes
     int bc = 0;
     for (int k = k0; k < k1; k++) bc += (sm.p[k] & 0xC000u) == 0xC000u;
@@ -475,16 +506,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws) {
         }
     }
     __syncthreads();
-    // ---- P4d: outputs -- component of every run (for K5) and the nodes of the
-    // border pixels (for K2)
-#pragma unroll
-    for (int i = 0; i < S; i++) {
-        const int rl = r0 + i;
-        if (rl >= rows) break;
-        const int b = sm.rowbase[rl], n = sm.nrun[rl];
-        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
-        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(b + o);
-    }
+    if (stop <= 6) return;
+    // ---- P4d: nodes of the border pixels (for K2)
     {
         const int ntop = sm.nrun[0], bb = sm.rowbase[rows - 1], nbot = sm.nrun[rows - 1];
         for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[tile * MAXRUN + o] = compnode[comp_of(o)];
@@ -535,11 +558,20 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             int nx = top[run_ord(X.hx, X.base, b)];
             gunion(ws.gparent, ws.gkey, nu, nx);
         }
-        m = first_in_run(u & dilate(X), u);
+        // upper runs whose leftmost lower neighbour has another leftmost upper
+        // neighbour (see upper_merge_heads / hole_bridged in K1)
+        {
+            const uint32_t t = x & dilate(U);
+            const uint32_t s = smear_up(t, x);
+            const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
+            const uint32_t S_ = s | (cin ? (x & ~(x + 1)) : 0u);
+            const uint32_t d = gword < g.WW ? ws.bm[(int64_t)(ru - 1) * g.WW + gword] : 0u;
+            m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_) & ~hole_bridged(u, U.xp, d);
+        }
         while (m) {
             int b = __ffs(m) - 1;
             m &= m - 1;
-            int q = 32 * lane + b + leftmost3(x, X.xp, X.xn, b);
+            int q = 32 * lane + b - 1;  // lower pixel h-1
             int lq = q >> 5;
             int nx = top[run_ord(shd[wib][1][lq], sbs[wib][1][lq], q & 31)];
             int nu = bot[run_ord(U.hx, U.base, b)];
@@ -798,6 +830,7 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
 
 // ==================================================================== host
 static bool g_attr_done = false;
+int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a phase (timing only)
 
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
@@ -819,7 +852,7 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, k1smem, stream>>>(img, g, ws);
+    k_tile_local<<<g.nT, NW * 32, k1smem, stream>>>(img, g, ws, g_k1_stop, g_k1_exper);
     mark(K_BORDER);
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
