@@ -41,7 +41,7 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         nT * CAPC * 4,                  // comprank
         nT * CAPC * 4,                  // complab
         nT * CAPB * 4,                  // gparent
-        nT * CAPB * 4,                  // gkey
+        nT * CAPB * 8,                  // gkey
         nT * CAPB * 4,                  // gnodeseg
         nT * CAPB * 4,                  // gnoderank
         nT * MAXRUN * 4,                // topnode
@@ -74,7 +74,7 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.comprank = reinterpret_cast<uint32_t *>(b + offs[A_COMPRANK]);
     w.complab = reinterpret_cast<int32_t *>(b + offs[A_COMPLAB]);
     w.gparent = reinterpret_cast<int32_t *>(b + offs[A_GPARENT]);
-    w.gkey = reinterpret_cast<int32_t *>(b + offs[A_GKEY]);
+    w.gkey = reinterpret_cast<int64_t *>(b + offs[A_GKEY]);
     w.gnodeseg = reinterpret_cast<int32_t *>(b + offs[A_GNODESEG]);
     w.gnoderank = reinterpret_cast<int32_t *>(b + offs[A_GNODERANK]);
     w.topnode = reinterpret_cast<int32_t *>(b + offs[A_TOP]);

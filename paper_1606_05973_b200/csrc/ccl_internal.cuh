@@ -39,12 +39,12 @@ struct Geometry {
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
     uint16_t *runcomp;    // [H][nTx][MAXRUN]  tile component of each run of each tile row
-    int32_t *compkey;     // [nT][CAPC]        raster index of the component's first pixel
+    int32_t *compkey;     // [nT][CAPC]        (row << 16 | run ordinal) of the component's root run
     int32_t *compnode;    // [nT][CAPC]        border-node id, or -1 (component inside the tile)
     uint32_t *comprank;   // [nT][CAPC]        (row<<16 | rank within its segment) for global roots
     int32_t *complab;     // [nT][CAPC]        final label of the component
     int32_t *gparent;     // [nT][CAPB]        global union-find over border components
-    int32_t *gkey;        // [nT][CAPB]        raster key of the node's first pixel
+    int64_t *gkey;        // [nT][CAPB]        (image row, tile column, run ordinal) key: raster order
     int32_t *gnodeseg;    // [nT][CAPB]        segment of a root node's first pixel
     int32_t *gnoderank;   // [nT][CAPB]        rank of a root node inside that segment
     int32_t *topnode;     // [nT][MAXRUN]      node of each run of the tile's first row
@@ -63,7 +63,7 @@ Geometry make_geometry(int H, int W);
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 
-enum { K_TILE = 0, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
+enum { K_PACK = 0, K_TILE, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it

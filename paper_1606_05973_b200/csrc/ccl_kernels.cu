@@ -1,8 +1,8 @@
 // ccl_kernels.cu -- B200 (sm_100a) kernels of the two-pass 8-connectivity CCL
 // pipeline.  DESIGN.md explains the design; paper citations are PAPER.md lines.
 //
-//   K1 k_tile_local   one CTA per 32x1024 tile.  128-bit streaming loads of the
-//                     image, packed into 32-bit row masks; the runs of the tile
+//   K0 k_pack         image -> 1 bit per pixel (128-bit streaming loads).
+//   K1 k_tile_local   one CTA per 32x1024 tile of row masks; the runs of the tile
 //                     are its provisional labels (index order = raster order).
 //                     Scan: every run copies its leftmost upper neighbour's
 //                     label (Scan_ARemSP's copy), 8 strips
@@ -31,8 +31,8 @@ namespace cclb {
 
 #define FULL 0xFFFFFFFFu
 
-const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_roots", "k_scan",
-                                           "k_final", "k_write"};
+const char *const kKernelNames[K_COUNT] = {"k_pack", "k_tile_local", "k_border", "k_roots",
+                                           "k_scan", "k_final", "k_write"};
 
 // ===================================================================== helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -196,7 +196,7 @@ __device__ __forceinline__ int gfind_ro(const int32_t *par, int x) {
     }
 }
 // Links the root with the larger key under the root with the smaller key.
-__device__ void gunion(int32_t *par, const int32_t *key, int a, int b) {
+__device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
     while (true) {
         a = gfind(par, a);
         b = gfind(par, b);
@@ -229,6 +229,18 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
     int n = min(32, g.W - col0);
     for (int i = 0; i < n; i++) m |= (uint32_t)(__ldcs(src + i) != 0) << i;
     return m;
+}
+
+// ========================================================================= K0
+// Foreground predicate (reading A10: byte != 0), packed to
+// one bit per pixel: thread = one 32-pixel word of the bitmask.  Streaming,
+// bandwidth-bound: the image is read exactly once here.
+__global__ void __launch_bounds__(256)
+k_pack(const uint8_t *__restrict__ img, Geometry g, uint32_t *__restrict__ bm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)g.H * g.WW) return;
+    const int row = (int)(i / g.WW), word = (int)(i % g.WW);
+    __stcg(bm + i, load_word(img, g, row, 32 * word));
 }
 
 // ========================================================================= K1
@@ -267,7 +279,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int *scratch, int &total) 
     return pre + off;
 }
 
-// Upper-side edges that the hook step does not already cover.  The edge set
+// Upper-side edges that the copy step does not already cover.  The edge set
 // {(L, leftmost upper run of L)} U {(U, leftmost lower run of U)} connects
 // everything two adjacent rows connect; the second family is redundant unless
 // U's head h touches the lower run L through pixel h-1 AND L reaches an upper
@@ -296,12 +308,8 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
     return ((u << 2) | (up >> 30)) & ((d << 1) | (dp >> 31));
 }
 
-__device__ __forceinline__ int run_index(const K1Smem &sm, int r, int lane_word, int bit) {
-    return sm.rowbase[r] + sm.hbase[r][lane_word] + __popc(sm.hd[r][lane_word] & upto(bit)) - 1;
-}
-
 __global__ void __launch_bounds__(NW * 32, 4)
-k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop, int exper) {
+k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
 
@@ -315,11 +323,12 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
     const int r0 = w * S;
     volatile uint16_t *vp = sm.p;
 
-    // ---- P0: image -> row masks, run heads, per-word run counts
+    // ---- P0: row masks (from K0), run heads, per-word run counts
     {
         uint32_t xs[S];
 #pragma unroll
-        for (int i = 0; i < S; i++) xs[i] = (r0 + i < rows) ? load_word(img, g, R0 + r0 + i, C0 + 32 * lane) : 0u;
+        for (int i = 0; i < S; i++)
+            xs[i] = (r0 + i < rows && gword < g.WW) ? __ldcg(ws.bm + (int64_t)(R0 + r0 + i) * g.WW + gword) : 0u;
 #pragma unroll
         for (int i = 0; i < S; i++) {
             const int rl = r0 + i;
@@ -332,7 +341,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
             sm.hd[rl][lane] = hx;
             sm.hbase[rl][lane] = (uint16_t)base;
             if (lane == 0) sm.nrun[rl] = (int)nr;
-            if (rl < rows && gword < g.WW) ws.bm[(int64_t)(R0 + rl) * g.WW + gword] = x;
         }
     }
     __syncthreads();
@@ -344,8 +352,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
     }
     __syncthreads();
     const int R = sm.rowbase[TH];
-
     if (stop <= 0) return;
+
     // ---- P2a: scan.  Every run starts as a new label; a
     // run with a foreground pixel among the three above any of its pixels
     // instead copies its leftmost upper neighbour's label (the decision
@@ -373,13 +381,19 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         const uint32_t xp = lane == 0 ? 0u : xpr;
         const uint32_t up = lane == 0 ? 0u : upr, un = lane == 31 ? 0u : unr;
         const uint32_t hx = sm.hd[rl][lane];
-        const uint32_t t = x & (u | (u << 1) | (up >> 31) | (u >> 1) | (un << 31));
+        // upper row: heads and run-index base of lanes lane-1, lane, lane+1
+        const uint32_t hu = sm.hd[rl - 1][lane];
+        const int ub = sm.rowbase[rl - 1] + sm.hbase[rl - 1][lane];
+        const uint32_t hup = __shfl_up_sync(FULL, hu, 1), hun = __shfl_down_sync(FULL, hu, 1);
+        const int ubp = __shfl_up_sync(FULL, ub, 1), ubn = __shfl_down_sync(FULL, ub, 1);
+        const uint32_t uL = (u << 1) | (up >> 31);  // upper pixel at p-1
+        const uint32_t t = x & (u | uL | (u >> 1) | (un << 31));
         const uint32_t s = smear_up(t, x);
         const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
         const uint32_t lead = x & ~(x + 1);
         const uint32_t S_ = s | (cin ? lead : 0u);
         uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
-        uint32_t mc = upper_merge_heads(sm.hd[rl - 1][lane], u, up, x, xp, S_);
+        uint32_t mc = upper_merge_heads(hu, u, up, x, xp, S_);
         if (rl >= 2) mc &= ~hole_bridged(u, up, sm.bm[rl - 2][lane]);
         sm.mc[rl][lane] = mc;
         const int lbase = rb + sm.hbase[rl][lane] - 1;
@@ -388,48 +402,59 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         while (ft) {
             const int b = __ffs(ft) - 1;
             ft &= ft - 1;
-            const int q = 32 * lane + b + leftmost3(u, up, un, b);
-            const int ui = run_index(sm, rl - 1, q >> 5, q & 31);
+            // leftmost upper foreground pixel among p-1, p, p+1 and its run
+            int ui;
+            if ((uL >> b) & 1u) {
+                ui = b == 0 ? ubp + __popc(hup) - 1 : ub + __popc(hu & upto(b - 1)) - 1;
+            } else if ((u >> b) & 1u) {
+                ui = ub + __popc(hu & upto(b)) - 1;
+            } else {
+                ui = b == 31 ? ubn + (int)(hun & 1u) - 1 : ub + __popc(hu & upto(b + 1)) - 1;
+            }
             vp[lbase + __popc(hx & upto(b))] = instrip ? vp[ui] : (uint16_t)ui;
         }
         __syncwarp();
     }
     __syncthreads();
-    if (stop <= 1) return;
-    // ---- P3a: resolve the hooks: a chain crosses at most one run per strip
-    // above, so a find per run is short; runs point at their roots afterwards
-    // (Alg. flatten's p[i] <- p[p[i]]).
-    const int per = (R + NW * 32 - 1) / (NW * 32);
-    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
-    for (int k = k0; k < k1; k++) {
-        uint32_t r = vp[k];
-        while (vp[r] != r) r = vp[r];
-        vp[k] = (uint16_t)r;
+    // ---- P3a: resolve the copies across strips, strip by strip (Alg. flatten's
+    // increasing order): a run of strip s points at a root of
+    // strip s or at a run of strip s-1, which is final once strip s-1 is done.
+    for (int st = 1; st < NW; st++) {
+        const int kb = sm.rowbase[min(st * S, TH)], ke = sm.rowbase[min(st * S + S, TH)];
+        for (int k = kb + (int)threadIdx.x; k < ke; k += NW * 32) {
+            const uint32_t pk = vp[k];
+            if ((int)pk < kb) vp[k] = vp[pk];
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    if (stop <= 2) return;
+    if (stop <= 1) return;
     // ---- P2b: the remaining edges, merged with lock-free Rem's splicing
-    // (the decision tree's copy(c,a)/copy(c,d) merges);
-    // most candidates already share a root.
+    // (the decision tree's copy(c,a)/copy(c,d) merges)
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
-        if (exper == 2) m = 0;
+        if (m == 0u) continue;
+        const uint32_t hu = sm.hd[rl - 1][lane];
+        const int ub = sm.rowbase[rl - 1] + sm.hbase[rl - 1][lane];
+        const int xb = sm.rowbase[rl] + sm.hbase[rl][lane];
+        const uint32_t hx = sm.hd[rl][lane];
         while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
-            const int q = 32 * lane + b - 1;  // lower pixel h-1 of the run below
-            const int a = run_index(sm, rl - 1, lane, b);
-            const int c = run_index(sm, rl, q >> 5, q & 31);
-            if (vp[a] != vp[c] && exper != 1) merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
+            const int a = ub + __popc(hu & upto(b)) - 1;  // the upper run with head h
+            // the lower run containing pixel h-1
+            const int c = b == 0 ? xb - 1 : xb + __popc(hx & upto(b - 1)) - 1;
+            if (vp[a] != vp[c]) merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
         }
     }
     __syncthreads();
-    if (stop <= 3) return;
-    // ---- P3b/P4a: final compression; roots in index order = raster order of
-    // first pixels get the consecutive component numbers (Alg. flatten's k++,
-    // PAPER.md:714-715)
+    if (stop <= 2) return;
+    // ---- P3: flatten -- every run -> its root (Alg. flatten's p[i] <- p[p[i]],
+    // PAPER.md:711-712); roots in index order = raster order of first pixels
+    // get the consecutive component numbers (Alg. flatten's k++)
+    const int per = (R + NW * 32 - 1) / (NW * 32);
+    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
     int cnt = 0;
     for (int k = k0; k < k1; k++) {
         uint32_t r = vp[k];
@@ -439,9 +464,23 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
     }
     int ncomp;
     int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
-    for (int k = k0; k < k1; k++)
-        if (sm.p[k] == (uint16_t)k) sm.p[k] = (uint16_t)(0x8000 | cidx++);  // root: flag | component
+    // component key = (row, ordinal) of the root run's head: ordered like the
+    // raster index of the component's first pixel
+    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
+    {
+        int rl = 0;  // row of run k0: the last row whose base is <= k0
+#pragma unroll
+        for (int step = TH / 2; step > 0; step >>= 1)
+            if (sm.rowbase[rl + step] <= k0) rl += step;
+        for (int k = k0; k < k1; k++) {
+            if (sm.p[k] != (uint16_t)k) continue;
+            while (sm.rowbase[rl + 1] <= k) rl++;
+            compkey[cidx] = (rl << 16) | (k - sm.rowbase[rl]);
+            sm.p[k] = (uint16_t)(0x8000 | cidx++);  // root: flag | component
+        }
+    }
     __syncthreads();
+    if (stop <= 3) return;
     auto comp_of = [&](int k) -> int {
         const uint32_t pk = sm.p[k];
         return (int)((pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu));
@@ -450,27 +489,15 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         const uint32_t pk = sm.p[k];
         return (pk & 0x8000u) ? k : (int)pk;
     };
-    if (stop <= 4) return;
-    // ---- P4b: per run head: its component (output for K5), and for root
-    // runs the component key = raster index of the head (the first pixel);
-    // mark components that touch the tile border (flag 0x4000 on the root)
-    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
+    // ---- P4a: component of every run (for K5); mark the components that
+    // touch the tile border (flag 0x4000 on the root)
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         if (rl >= rows) break;
-        uint32_t hm = sm.hd[rl][lane];
-        int o = sm.hbase[rl][lane];
-        const int rb = sm.rowbase[rl];
+        const int b = sm.rowbase[rl], n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
-        while (hm) {
-            const int b = __ffs(hm) - 1;
-            hm &= hm - 1;
-            const uint32_t pk = sm.p[rb + o];
-            const uint32_t c = (pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu);
-            dst[o++] = (uint16_t)c;
-            if (pk & 0x8000u) compkey[c] = (R0 + rl) * g.W + C0 + 32 * lane + b;
-        }
+        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(b + o);
     }
     auto mark = [&](int k) {
         const int r = root_of(k);
@@ -484,8 +511,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         if ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) mark(sm.rowbase[r + 1] - 1);
     }
     __syncthreads();
-    if (stop <= 5) return;
-    // ---- P4c: border components -> global union-find nodes
+    if (stop <= 4) return;
+    // ---- P4b: border components -> global union-find nodes
     int bc = 0;
     for (int k = k0; k < k1; k++) bc += (sm.p[k] & 0xC000u) == 0xC000u;
     int nborder;
@@ -498,16 +525,18 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         const int c = (int)(pk & 0x3FFFu);
         if (pk & 0x4000u) {
             const int node = nodebase + bidx++;
+            const int key = compkey[c];
             compnode[c] = node;
             ws.gparent[node] = node;
-            ws.gkey[node] = compkey[c];
+            // global order = (image row, tile column, run ordinal): raster order
+            ws.gkey[node] = ((int64_t)(R0 + (key >> 16)) * g.nTx + tx) * MAXRUN + (key & 0xFFFF);
         } else {
             compnode[c] = -1;
         }
     }
     __syncthreads();
-    if (stop <= 6) return;
-    // ---- P4d: nodes of the border pixels (for K2)
+    if (stop <= 5) return;
+    // ---- P4c: nodes of the border pixels (for K2)
     {
         const int ntop = sm.nrun[0], bb = sm.rowbase[rows - 1], nbot = sm.nrun[rows - 1];
         for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[tile * MAXRUN + o] = compnode[comp_of(o)];
@@ -627,7 +656,7 @@ k_roots(Geometry g, Workspace ws) {
         const int c = c0 + lane;
         if (c < ncomp) {
             const int node = compnode[c];
-            if (node < 0 || __ldcg(ws.gparent + node) == node) atomicAdd(&c_row[compkey[c] / g.W - R0], 1);
+            if (node < 0 || __ldcg(ws.gparent + node) == node) atomicAdd(&c_row[compkey[c] >> 16], 1);
         }
     }
     __syncwarp();
@@ -647,7 +676,7 @@ k_roots(Geometry g, Workspace ws) {
         if (c < ncomp) {
             node = compnode[c];
             root = node < 0 || __ldcg(ws.gparent + node) == node;
-            rl = compkey[c] / g.W - R0;
+            rl = compkey[c] >> 16;
         }
         const uint32_t bal = __ballot_sync(FULL, root);
         if (c < ncomp) {
@@ -835,7 +864,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+    return 6 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
@@ -851,8 +880,13 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };
+    mark(K_PACK);
+    {
+        const int64_t words = (int64_t)g.H * g.WW;
+        k_pack<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(img, g, ws.bm);
+    }
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, k1smem, stream>>>(img, g, ws, g_k1_stop, g_k1_exper);
+    k_tile_local<<<g.nT, NW * 32, k1smem, stream>>>(g, ws, g_k1_stop, g_k1_exper);
     mark(K_BORDER);
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;

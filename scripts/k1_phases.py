@@ -7,10 +7,10 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c4_voronoi_21600"
 img = torch.from_numpy(synth.generate(name)).cuda()
 plan = ccl.Plan(*img.shape)
 out = torch.empty(img.shape, dtype=torch.int32, device="cuda"); n = torch.empty(1, dtype=torch.int32, device="cuda")
-for stop, ex in [(2, 0), (3, 0), (3, 1), (3, 2), (99, 0)]:
+for stop, ex in [(0, 0), (1, 0), (2, 0), (3, 0), (4, 0), (5, 0), (99, 0)]:
     ccl._L.ccl_debug_set(1, stop); ccl._L.ccl_debug_set(2, ex)
     plan.set_profiling(20)
     for _ in range(23): plan.label(img, out, n)
     t = plan.kernel_times()
-    print(f"{name} stop={stop:2d} exper={ex} k_tile_local {t['k_tile_local']*1000:8.1f} us")
+    print(f"{name} stop={stop:2d} k_pack {t['k_pack']*1000:7.1f} us  k_tile_local {t['k_tile_local']*1000:8.1f} us  total {sum(t.values())*1000:8.1f} us")
 ccl._L.ccl_debug_set(1, 99); ccl._L.ccl_debug_set(2, 0)
