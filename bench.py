@@ -247,21 +247,33 @@ def main():
 
     peak, peak_src = peak_hbm()
     roofline = None
-    ktimes = None
     if plan is not None:
         ktimes = plan.kernel_times()
         plan.set_profiling(0)
-        dom = max(("k_pack", "k_write"), key=lambda k: ktimes[k])
-        alg = ALG_BYTES_PER_PX[dom] * H * W
-        ach = alg / (ktimes[dom] * 1e-3) / 1e9
-        traffic = ncu_traffic(dom, args.workload)
-        path_ach = ALG_BYTES_PER_PX["path"] * H * W / (ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": traffic,
-                    "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
-                    "kernel_ms": ktimes,
-                    "path": {"achieved": path_ach, "frac": path_ach / peak,
-                             "algorithmic_bytes_per_step": ALG_BYTES_PER_PX["path"] * H * W}}
+        # The path is HBM-bound by its algorithmic bytes (SURVEY.md section 8(d):
+        # 1 B read + 4 B written per pixel); the roofline is reported for the
+        # whole step -- the unit one launch sequence processes -- with every
+        # kernel's own share beside it.
+        alg = ALG_BYTES_PER_PX["path"] * H * W
+        ach = alg / (ms * 1e-3) / 1e9
+        dom = max(ktimes, key=ktimes.get)
+        kern = {}
+        for k, t in ktimes.items():
+            e = {"ms": t, "share": t / sum(ktimes.values())}
+            if ALG_BYTES_PER_PX.get(k):
+                e["algorithmic_bytes"] = ALG_BYTES_PER_PX[k] * H * W
+                e["achieved_gbs"] = e["algorithmic_bytes"] / (t * 1e-3) / 1e9
+                e["frac"] = e["achieved_gbs"] / peak
+            tr = ncu_traffic(k, args.workload)
+            if tr is not None:
+                e["ncu_dram_bytes"] = tr
+            kern[k] = e
+        tr_all = [ncu_traffic(k, args.workload) for k in ktimes]
+        roofline = {"bound": "hbm", "kernel": "path (all kernels of one step)", "achieved": ach,
+                    "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": sum(tr_all) if all(t is not None for t in tr_all) else None,
+                    "algorithmic_bytes_per_step": alg, "peak_source": peak_src,
+                    "dominant_kernel": dom, "kernels": kern}
 
     line = {
         "metric": METRIC, "value": value, "unit": "Gpx/s", "n_gpus": ws, "steps": args.steps,
