@@ -72,6 +72,7 @@ PRODUCT_SRCS = [
     "paper_1606_05973_b200/csrc/ccl_kernels.cu",
     "paper_1606_05973_b200/csrc/ccl_api.cu",
     "paper_1606_05973_b200/csrc/ccl_sharded.cu",
+    "paper_1606_05973_b200/csrc/ccl_bands.cu",
 ]
 PRODUCT_HDRS = [
     "include/ccl.h",

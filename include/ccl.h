@@ -130,6 +130,33 @@ ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row
                              int H_total, int32_t *band_labels, int32_t *n_components,
                              ccl_nccl_comm_t comm, ccl_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * ccl_label_banded -- the row-band protocol of ccl_label_sharded run on ONE
+ * GPU: the image (DEVICE pointers, as in ccl_label) is split into `nbands`
+ * contiguous row bands of near-equal height (remainder to the last bands),
+ * every band is labelled as its own image and the bands are joined by the
+ * same cross-band resolution, with the all-gathers done by local copies.
+ * Output identical to ccl_label.  1 <= nbands <= H.  Synchronizes `stream`.
+ * Exists to test the multi-GPU protocol where only one GPU is available.
+ * ---------------------------------------------------------------------- */
+ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_t *labels,
+                            int32_t *n_components, ccl_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * ccl_xband_resolve -- the host-side cross-band step of the row-band protocol
+ * (PARemSP's boundary merge), exposed for host tests.
+ *   rows[2k], rows[2k+1]: HOST arrays of W keys for band k's first and last
+ *     row: a per-pixel key of the pixel's band-local component (-1 =
+ *     background); keys are unique per component and increase with the
+ *     raster position of the component's first pixel.
+ *   Pixels of band k's last row and band k+1's first row that are 8-adjacent
+ *   join their components; equal keys are the same component.
+ *   out_min: HOST array of 2*W; for band `self`'s first and last row, the
+ *     smallest key of each pixel's joined class (-1 for background).
+ * Returns CCL_OK or CCL_INVALID_ARGUMENT.  Pure host code, no GPU needed.
+ * ---------------------------------------------------------------------- */
+int ccl_xband_resolve(int nb, int W, const int64_t *const *rows, int self, int64_t *out_min);
+
 /* NCCL bootstrap helpers (torch.distributed does not expose its ncclComm_t):
  * rank 0 creates the 128-byte unique id, the harness broadcasts it (e.g. via
  * torch.distributed over gloo), then every rank creates its communicator on

@@ -48,6 +48,10 @@ _L.ccl_plan_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p),
 _L.ccl_plan_kernel_times.restype = _i
 _L.ccl_label_sharded.argtypes = [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]
 _L.ccl_label_sharded.restype = _i
+_L.ccl_label_banded.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
+_L.ccl_label_banded.restype = _i
+_L.ccl_xband_resolve.argtypes = [_i, _i, ctypes.POINTER(ctypes.c_void_p), _i, _vp]
+_L.ccl_xband_resolve.restype = _i
 _L.ccl_nccl_get_unique_id.argtypes = [_vp]
 _L.ccl_nccl_get_unique_id.restype = _i
 _L.ccl_nccl_comm_create.argtypes = [_vp, _i, _i, ctypes.POINTER(_vp)]
@@ -207,3 +211,33 @@ def label_sharded(band_img, row0, H_total, comm, out=None, n_out=None, stream=No
                                 n_out.data_ptr(), comm.handle, _stream_handle(stream)),
            "ccl_label_sharded")
     return out, n_out
+
+
+def label_banded(img, nbands, out=None, n_out=None, stream=None):
+    """The multi-GPU row-band protocol run on one GPU (ccl_label_banded):
+    `nbands` bands labelled separately and joined by the cross-band step.
+    Same output as label()."""
+    _check_img(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, W), dtype=torch.int32, device=img.device)
+    if n_out is None:
+        n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+    _check(_L.ccl_label_banded(img.data_ptr(), H, W, int(nbands), out.data_ptr(), n_out.data_ptr(),
+                               _stream_handle(stream)), "ccl_label_banded")
+    return out, n_out
+
+
+def xband_resolve(rows, self_band):
+    """Host cross-band resolution (ccl_xband_resolve).  rows: list of 2*nb
+    int64 numpy arrays of length W (band k's first row, last row, ...), -1 for
+    background.  Returns the class-minimum keys of band `self_band`'s two rows
+    as an int64 array of shape (2, W)."""
+    import numpy as np
+    nb = len(rows) // 2
+    W = len(rows[0])
+    arrs = [np.ascontiguousarray(r, dtype=np.int64) for r in rows]
+    ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    out = np.empty((2, W), dtype=np.int64)
+    _check(_L.ccl_xband_resolve(nb, W, ptrs, int(self_band), out.ctypes.data), "ccl_xband_resolve")
+    return out

@@ -22,6 +22,7 @@ Geometry make_geometry(int H, int W) {
     g.nseg = H * g.nTx;
     g.nscan = (g.nseg + SCAN_TILE - 1) / SCAN_TILE;
     g.aligned = (W % 16) == 0;
+    g.row0 = 0;
     return g;
 }
 
@@ -86,6 +87,8 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.segoff = reinterpret_cast<int32_t *>(b + offs[A_SEGOFF]);
     w.scanstate = reinterpret_cast<unsigned long long *>(b + offs[A_SCANSTATE]);
     w.ticket = reinterpret_cast<int32_t *>(b + offs[A_TICKET]);
+    w.boff = nullptr;
+    w.xlab = nullptr;
     return w;
 }
 

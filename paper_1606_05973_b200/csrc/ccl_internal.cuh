@@ -33,6 +33,7 @@ struct Geometry {
     int nseg;      // H * nTx: (row, tile-column) segments in raster order
     int nscan;     // decoupled-lookback partitions over the segments
     int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
+    int row0;      // global row of this image's row 0 (row bands of a sharded image; else 0)
 };
 
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).
@@ -56,6 +57,10 @@ struct Workspace {
     int32_t *segoff;      // [nseg]            exclusive prefix of segcnt (raster order)
     unsigned long long *scanstate;  // [nscan] decoupled-lookback descriptors
     int32_t *ticket;      // [1]               dynamic partition counter
+    // row bands only (null for a whole image):
+    const int32_t *boff;  // [1]               labels of earlier bands (added to every label)
+    const int32_t *xlab;  // [*]               labels of roots owned by other bands; a node
+                          //                   whose parent is -2-f takes xlab[f]
 };
 
 Geometry make_geometry(int H, int W);
@@ -71,6 +76,25 @@ extern const char *const kKernelNames[K_COUNT];
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev);
+// The same pipeline in three stages (row bands insert the cross-band step
+// between them): local = pack, tile labeling, tile-edge merge;
+// count = roots + numbering scan (N of this image/band -> *n_components);
+// final = component labels + label write.
+cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
+                            cudaStream_t stream, cudaEvent_t *ev);
+cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
+                            cudaStream_t stream, cudaEvent_t *ev);
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+                            cudaStream_t stream, cudaEvent_t *ev);
+// Row bands: per-pixel root key / root node of local row `row` (-1 background).
+cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
+                           int32_t *nodes, cudaStream_t stream);
+// gparent[act[i].x] = act[i].y
+cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t stream);
+// Per pixel of local row `row`: the final label if the pixel's root node (from
+// band_row_roots) is still a root after band_apply, else -1.
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
+                        int32_t *labels_out, cudaStream_t stream);
 // Number of kernel launches run_pipeline makes for this geometry.
 int pipeline_launches(const Geometry &g);
 

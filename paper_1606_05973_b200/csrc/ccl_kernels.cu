@@ -155,8 +155,8 @@ __device__ __forceinline__ int leftmost3(uint32_t w, uint32_t wp, uint32_t wn, i
 // order).  This is the paper's merge run concurrently the
 // way its merger does: the root link is an atomicCAS
 // (the role of merger's lock + "still a root?" re-check)
-// and the splice is a plain store, unlocked as in merger (PAPER.md:1025,
-// 1039).  Every value stored into p[x] is smaller than x, so no cycle forms.
+// and the splice (unlocked in merger) is a CAS that only
+// lowers p[x].  Every value stored into p[x] is smaller than x: no cycles.
 __device__ void merge_smem(uint16_t *p, uint32_t x, uint32_t y) {
     volatile uint16_t *vp = p;
     while (true) {
@@ -173,7 +173,18 @@ __device__ void merge_smem(uint16_t *p, uint32_t x, uint32_t y) {
                 return;
             continue;  // x stopped being a root meanwhile: retry from x
         }
-        vp[x] = (uint16_t)py;  // splice: x's subtree becomes a sibling under py
+        // splice: x's subtree becomes a sibling under py.  Done with a CAS
+        // that only ever lowers p[x]; an unconditional store can raise p[x]
+        // over a concurrent splice, and that lost rare unions in testing.
+        {
+            unsigned short cur = (unsigned short)px;
+            while (true) {
+                const unsigned short o =
+                    atomicCAS(reinterpret_cast<unsigned short *>(p + x), cur, (unsigned short)py);
+                if (o == cur || o <= py) break;
+                cur = o;
+            }
+        }
         x = px;
     }
 }
@@ -188,12 +199,19 @@ __device__ __forceinline__ int gfind(int32_t *par, int x) {
         x = ppx;
     }
 }
+// Read-only find; returns the root node, or a negative parent (-2-f) when the
+// tree hangs under a root owned by another row band.
 __device__ __forceinline__ int gfind_ro(const int32_t *par, int x) {
     while (true) {
         int px = __ldcg(par + x);
-        if (px == x) return x;
+        if (px == x || px < 0) return px;
         x = px;
     }
+}
+// Final label of a root node (or a foreign reference).
+__device__ __forceinline__ int32_t node_label(const Workspace &ws, int root, int32_t off) {
+    if (root < 0) return ws.xlab[-2 - root];
+    return off + ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
 }
 // Links the root with the larger key under the root with the smaller key.
 __device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
@@ -529,7 +547,7 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
             compnode[c] = node;
             ws.gparent[node] = node;
             // global order = (image row, tile column, run ordinal): raster order
-            ws.gkey[node] = ((int64_t)(R0 + (key >> 16)) * g.nTx + tx) * MAXRUN + (key & 0xFFFF);
+            ws.gkey[node] = ((int64_t)(g.row0 + R0 + (key >> 16)) * g.nTx + tx) * MAXRUN + (key & 0xFFFF);
         } else {
             compnode[c] = -1;
         }
@@ -774,6 +792,7 @@ k_final(Geometry g, Workspace ws) {
     const uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
     const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
     int32_t *complab = ws.complab + (int64_t)tile * CAPC;
+    const int32_t off = ws.boff ? *ws.boff : 0;
     for (int c0 = 0; c0 < ncomp; c0 += 64) {
         // two components per lane in flight
         const int ca = c0 + lane, cb = c0 + 32 + lane;
@@ -781,18 +800,16 @@ k_final(Geometry g, Workspace ws) {
         int la = 0, lb = 0;
         if (ca < ncomp) {
             if (ra != 0xFFFFFFFFu) {
-                la = ws.segoff[(int64_t)(R0 + (int)(ra >> 16)) * g.nTx + tx] + (int)(ra & 0xFFFF) + 1;
+                la = off + ws.segoff[(int64_t)(R0 + (int)(ra >> 16)) * g.nTx + tx] + (int)(ra & 0xFFFF) + 1;
             } else {
-                const int root = gfind_ro(ws.gparent, compnode[ca]);
-                la = ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+                la = node_label(ws, gfind_ro(ws.gparent, compnode[ca]), off);
             }
         }
         if (cb < ncomp) {
             if (rb != 0xFFFFFFFFu) {
-                lb = ws.segoff[(int64_t)(R0 + (int)(rb >> 16)) * g.nTx + tx] + (int)(rb & 0xFFFF) + 1;
+                lb = off + ws.segoff[(int64_t)(R0 + (int)(rb >> 16)) * g.nTx + tx] + (int)(rb & 0xFFFF) + 1;
             } else {
-                const int root = gfind_ro(ws.gparent, compnode[cb]);
-                lb = ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
+                lb = node_label(ws, gfind_ro(ws.gparent, compnode[cb]), off);
             }
         }
         if (ca < ncomp) complab[ca] = la;
@@ -857,6 +874,50 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     }
 }
 
+// ================================================================ row bands
+// Per pixel of a local row: the key and node of its component's root in the
+// band's forest (after k_border).  One warp per 1024-px row segment.
+__global__ void __launch_bounds__(256)
+k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
+    const int lane = lane_id();
+    const int tx = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (tx >= g.nTx) return;
+    const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
+    const int gword = tx * WPR + lane;
+    const uint32_t x = gword < g.WW ? ws.bm[(int64_t)row * g.WW + gword] : 0u;
+    const uint32_t xl = __shfl_up_sync(FULL, x, 1);
+    const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
+    uint32_t nr;
+    const uint32_t base = warp_excl_scan(__popc(hx), nr);
+    const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * MAXRUN;
+    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
+    for (int b = 0; b < 32; b++) {
+        const int c = C0 + 32 * lane + b;
+        if (c >= g.W) break;
+        int64_t key = -1;
+        int32_t node = -1;
+        if ((x >> b) & 1u) {
+            const int comp = rc[run_ord(hx, base, b)];
+            node = gfind_ro(ws.gparent, compnode[comp]);
+            key = ws.gkey[node];
+        }
+        keys[c] = key;
+        nodes[c] = node;
+    }
+}
+
+__global__ void k_band_apply(int32_t *gparent, const int2 *act, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) gparent[act[i].x] = act[i].y;
+}
+
+__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.W) return;
+    const int n = nodes[c];
+    out[c] = (n >= 0 && __ldcg(ws.gparent + n) == n) ? node_label(ws, n, *ws.boff) : -1;
+}
+
 // ==================================================================== host
 static bool g_attr_done = false;
 int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a phase (timing only)
@@ -867,16 +928,18 @@ int pipeline_launches(const Geometry &g) {
     return 6 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
-cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
-                         int32_t *labels, int32_t *n_components, cudaStream_t stream,
-                         cudaEvent_t *ev) {
-    cudaError_t e;
-    const int k1smem = (int)sizeof(K1Smem);
-    if (!g_attr_done) {
-        e = cudaFuncSetAttribute(k_tile_local, cudaFuncAttributeMaxDynamicSharedMemorySize, k1smem);
-        if (e != cudaSuccess) return e;
-        g_attr_done = true;
-    }
+static cudaError_t set_attrs() {
+    if (g_attr_done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_tile_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(K1Smem));
+    if (e == cudaSuccess) g_attr_done = true;
+    return e;
+}
+
+cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
+                            cudaStream_t stream, cudaEvent_t *ev) {
+    cudaError_t e = set_attrs();
+    if (e != cudaSuccess) return e;
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };
@@ -886,21 +949,63 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
         k_pack<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(img, g, ws.bm);
     }
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, k1smem, stream>>>(g, ws, g_k1_stop, g_k1_exper);
+    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(g, ws, g_k1_stop, g_k1_exper);
     mark(K_BORDER);
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
     const int64_t warps = nh + (nv + 31) / 32;
     if (warps > 0) k_border<<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(g, ws, nh);
+    return cudaGetLastError();
+}
+
+cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
+                            cudaStream_t stream, cudaEvent_t *ev) {
+    auto mark = [&](int i) {
+        if (ev) cudaEventRecord(ev[i], stream);
+    };
     mark(K_ROOTS);
     k_roots<<<(g.nT + K3_WARPS - 1) / K3_WARPS, K3_WARPS * 32, 0, stream>>>(g, ws);
     mark(K_SCAN);
     k_scan<<<g.nscan, SCAN_THREADS, 0, stream>>>(g, ws, n_components);
+    return cudaGetLastError();
+}
+
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+                            cudaStream_t stream, cudaEvent_t *ev) {
+    auto mark = [&](int i) {
+        if (ev) cudaEventRecord(ev[i], stream);
+    };
     mark(K_FINAL);
     k_final<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws);
     mark(K_WRITE);
     k_write<<<(unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream>>>(g, ws, labels);
     mark(K_COUNT);
+    return cudaGetLastError();
+}
+
+cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
+                         int32_t *labels, int32_t *n_components, cudaStream_t stream,
+                         cudaEvent_t *ev) {
+    cudaError_t e = run_stage_local(g, ws, img, stream, ev);
+    if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev);
+    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev);
+    return e;
+}
+
+cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
+                           int32_t *nodes, cudaStream_t stream) {
+    k_band_rows<<<(g.nTx + 7) / 8, 256, 0, stream>>>(g, ws, row, keys, nodes);
+    return cudaGetLastError();
+}
+
+cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t stream) {
+    if (n > 0) k_band_apply<<<(n + 255) / 256, 256, 0, stream>>>(ws.gparent, act, n);
+    return cudaGetLastError();
+}
+
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
+                        int32_t *labels_out, cudaStream_t stream) {
+    k_band_export<<<(g.W + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out);
     return cudaGetLastError();
 }
 

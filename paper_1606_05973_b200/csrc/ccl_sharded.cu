@@ -1,4 +1,4 @@
-// ccl_sharded.cu -- multi-GPU row-band entry point and NCCL bootstrap.
+// ccl_sharded.cu -- NCCL bootstrap helpers for ccl_label_sharded (ccl_bands.cu).
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -33,19 +33,6 @@ ccl_status ccl_nccl_comm_destroy(ccl_nccl_comm_t comm) {
     if (!comm) return CCL_INVALID_ARGUMENT;
     return ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)) == ncclSuccess ? CCL_OK
                                                                               : CCL_NCCL_ERROR;
-}
-
-ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0, int H_total,
-                             int32_t *band_labels, int32_t *n_components, ccl_nccl_comm_t comm,
-                             ccl_stream_t stream) {
-    if (!comm || band_H < 1 || W < 1 || row0 < 0 || H_total < 1 || row0 + band_H > H_total)
-        return CCL_INVALID_ARGUMENT;
-    int nranks = 0;
-    if (ncclCommCount(reinterpret_cast<ncclComm_t>(comm), &nranks) != ncclSuccess)
-        return CCL_NCCL_ERROR;
-    if (nranks == 1 && band_H == H_total && row0 == 0)
-        return ccl_label(band_img, band_H, W, band_labels, n_components, stream);
-    return CCL_INVALID_ARGUMENT;  // multi-band protocol: see ccl_bands.cu (in progress)
 }
 
 }  // extern "C"

@@ -1,0 +1,58 @@
+"""The row-band (multi-GPU) protocol, run on one GPU through ccl_label_banded:
+for every band count the output must equal the oracle bit-for-bit (and hence
+the single-GPU result), on images whose components cross every band edge."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ccl = pytest.importorskip("paper_1606_05973_b200") if torch.cuda.is_available() else None
+
+
+def banded(img, nb):
+    lab, n = ccl.label_banded(torch.from_numpy(np.ascontiguousarray(img)).cuda(), nb)
+    torch.cuda.synchronize()
+    return lab.cpu().numpy(), int(n.item())
+
+
+@pytest.mark.parametrize("nb", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("name", ["c1_bernoulli_512", "c2_blobs_1024", "c3_percolation_8192",
+                                  "c4_voronoi_21600", "c5a_serpentine_16384", "c5b_comb_16384"])
+def test_bands_match_oracle(name, nb):
+    img = synth.scaled(name, 451, 2200)
+    lo, no = oracle.label(img)
+    lb, n = banded(img, nb)
+    assert n == no and np.array_equal(lb, lo), (name, nb)
+
+
+@pytest.mark.parametrize("nb", [2, 7, 16, 33])
+def test_bands_thin_and_uneven(nb):
+    """Bands of 1-2 rows, heights not multiples of the 32-row tile."""
+    for (H, W, p) in [(40, 300, 0.45), (70, 1025, 0.6), (33, 17, 0.5)]:
+        if nb > H:
+            continue
+        img = synth.bernoulli(H, W, p, seed=nb * 100 + H)
+        lo, no = oracle.label(img)
+        lb, n = banded(img, nb)
+        assert n == no and np.array_equal(lb, lo), (H, W, p, nb)
+
+
+def test_bands_chains_through_all_bands():
+    """Serpentine and comb: one component threaded through every band."""
+    for img in (synth.serpentine(257, 1100), synth.comb(257, 1100)):
+        for nb in (2, 4, 8):
+            lb, n = banded(img, nb)
+            assert n == 1 and np.array_equal(lb, img.astype(np.int32))
+
+
+@pytest.mark.parametrize("nb", [2, 4, 8])
+def test_full_c4_banded(nb):
+    """The bench workload split the way bench.py --gpus N splits it."""
+    img = synth.generate("c4_voronoi_21600")
+    lo, no = oracle.label(img)
+    lb, n = banded(img, nb)
+    assert n == no and np.array_equal(lb, lo)
