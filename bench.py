@@ -213,7 +213,8 @@ def main():
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         comm = ccl.NcclComm(obj[0], ws, rank)
-        step = lambda: ccl.label_sharded(d_img, row0, H, comm, out, n_out)  # noqa: E731
+        splan = ccl.ShardPlan(bh, W, row0, H, comm)
+        step = lambda: splan.label(d_img, out, n_out)  # noqa: E731
         plan = None
         launches_per_step = None
 

@@ -130,6 +130,17 @@ ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row
                              int H_total, int32_t *band_labels, int32_t *n_components,
                              ccl_nccl_comm_t comm, ccl_stream_t stream);
 
+/* Sharded plans: the workspace and exchange buffers of one rank's band,
+ * created once (collective: every rank calls it; checks the band layout as
+ * ccl_label_sharded does) and reused by ccl_shard_plan_label, which has the
+ * contract of ccl_label_sharded.  ccl_label_sharded = create + label + destroy. */
+typedef struct ccl_shard_plan_st *ccl_shard_plan;
+ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_nccl_comm_t comm,
+                                 ccl_stream_t stream, ccl_shard_plan *plan_out);
+ccl_status ccl_shard_plan_label(ccl_shard_plan plan, const uint8_t *band_img, int32_t *band_labels,
+                                int32_t *n_components, ccl_stream_t stream);
+ccl_status ccl_shard_plan_destroy(ccl_shard_plan plan);
+
 /* ------------------------------------------------------------------------
  * ccl_label_banded -- the row-band protocol of ccl_label_sharded run on ONE
  * GPU: the image (DEVICE pointers, as in ccl_label) is split into `nbands`

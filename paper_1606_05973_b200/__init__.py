@@ -52,6 +52,12 @@ _L.ccl_label_banded.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
 _L.ccl_label_banded.restype = _i
 _L.ccl_xband_resolve.argtypes = [_i, _i, ctypes.POINTER(ctypes.c_void_p), _i, _vp]
 _L.ccl_xband_resolve.restype = _i
+_L.ccl_shard_plan_create.argtypes = [_i, _i, _i, _i, _vp, _vp, ctypes.POINTER(_vp)]
+_L.ccl_shard_plan_create.restype = _i
+_L.ccl_shard_plan_label.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_L.ccl_shard_plan_label.restype = _i
+_L.ccl_shard_plan_destroy.argtypes = [_vp]
+_L.ccl_shard_plan_destroy.restype = _i
 _L.ccl_nccl_get_unique_id.argtypes = [_vp]
 _L.ccl_nccl_get_unique_id.restype = _i
 _L.ccl_nccl_comm_create.argtypes = [_vp, _i, _i, ctypes.POINTER(_vp)]
@@ -241,3 +247,38 @@ def xband_resolve(rows, self_band):
     out = np.empty((2, W), dtype=np.int64)
     _check(_L.ccl_xband_resolve(nb, W, ptrs, int(self_band), out.ctypes.data), "ccl_xband_resolve")
     return out
+
+
+class ShardPlan:
+    """One rank's band of a row-sharded image (ccl_shard_plan_* in include/ccl.h).
+    Collective: every rank of `comm` creates its plan with the same W, H_total."""
+
+    def __init__(self, band_H, W, row0, H_total, comm, stream=None):
+        self.band_H, self.W, self.row0, self.H_total = int(band_H), int(W), int(row0), int(H_total)
+        self._p = ctypes.c_void_p()
+        _check(_L.ccl_shard_plan_create(self.band_H, self.W, self.row0, self.H_total, comm.handle,
+                                        _stream_handle(stream), ctypes.byref(self._p)),
+               "ccl_shard_plan_create")
+
+    def label(self, band_img, out=None, n_out=None, stream=None):
+        _check_img(band_img)
+        if tuple(band_img.shape) != (self.band_H, self.W):
+            raise ValueError("band shape mismatch")
+        if out is None:
+            out = torch.empty((self.band_H, self.W), dtype=torch.int32, device=band_img.device)
+        if n_out is None:
+            n_out = torch.empty(1, dtype=torch.int32, device=band_img.device)
+        _check(_L.ccl_shard_plan_label(self._p, band_img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
+                                       _stream_handle(stream)), "ccl_shard_plan_label")
+        return out, n_out
+
+    def close(self):
+        if self._p:
+            _L.ccl_shard_plan_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

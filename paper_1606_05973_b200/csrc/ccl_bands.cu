@@ -26,6 +26,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <new>
 #include <numeric>
 #include <unordered_map>
 #include <vector>
@@ -345,11 +346,31 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
     return CCL_OK;
 }
 
-ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0, int H_total,
-                             int32_t *band_labels, int32_t *n_components, ccl_nccl_comm_t comm_,
-                             ccl_stream_t stream) {
-    if (!comm_ || !band_img || !band_labels || !n_components || band_H < 1 || W < 1 || row0 < 0 ||
-        H_total < 1 || row0 + band_H > H_total)
+}  // extern "C"
+
+struct ccl_shard_plan_st {
+    Band b;
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0, W = 0;
+    int32_t total = 0;
+    int64_t *d_allkeys = nullptr;
+    int32_t *d_allexp = nullptr, *d_alln = nullptr;
+    std::vector<int64_t> allkeys;
+    std::vector<int32_t> allexp, nband;
+    ~ccl_shard_plan_st() {
+        if (d_allkeys) cudaFree(d_allkeys);
+        if (d_allexp) cudaFree(d_allexp);
+        if (d_alln) cudaFree(d_alln);
+    }
+};
+
+extern "C" {
+
+ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_nccl_comm_t comm_,
+                                 ccl_stream_t stream, ccl_shard_plan *plan_out) {
+    if (!plan_out) return CCL_INVALID_ARGUMENT;
+    *plan_out = nullptr;
+    if (!comm_ || band_H < 1 || W < 1 || row0 < 0 || H_total < 1 || row0 + band_H > H_total)
         return CCL_INVALID_ARGUMENT;
     if ((int64_t)H_total * W > INT32_MAX) return CCL_TOO_LARGE;
     ncclComm_t comm = reinterpret_cast<ncclComm_t>(comm_);
@@ -357,7 +378,6 @@ ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row
     int nranks = 0, rank = 0;
     CKN(ncclCommCount(comm, &nranks));
     CKN(ncclCommUserRank(comm, &rank));
-
     // collective argument check: every rank's (band_H, row0, W, H_total)
     int32_t *d_meta = nullptr;
     CK(cudaMalloc(&d_meta, sizeof(int32_t) * 4 * (nranks + 1)));
@@ -368,75 +388,109 @@ ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row
     CK(cudaMemcpyAsync(meta.data(), d_meta + 4, sizeof(int32_t) * 4 * nranks, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     cudaFree(d_meta);
-    std::vector<int> bh(nranks), r0(nranks);
     int acc = 0;
     bool ok = true;
     for (int k = 0; k < nranks; k++) {
-        bh[k] = meta[4 * k];
-        r0[k] = meta[4 * k + 1];
-        ok = ok && r0[k] == acc && meta[4 * k + 2] == W && meta[4 * k + 3] == H_total && bh[k] >= 1;
-        acc += bh[k];
+        ok = ok && meta[4 * k + 1] == acc && meta[4 * k + 2] == W && meta[4 * k + 3] == H_total &&
+             meta[4 * k] >= 1;
+        acc += meta[4 * k];
     }
     if (!ok || acc != H_total) return CCL_INVALID_ARGUMENT;
+    ccl_shard_plan p = new (std::nothrow) ccl_shard_plan_st;
+    if (!p) return CCL_OUT_OF_MEMORY;
+    p->comm = comm;
+    p->nranks = nranks;
+    p->rank = rank;
+    p->W = W;
+    ccl_status st = band_init(p->b, band_H, W, row0);
+    if (st != CCL_OK) {
+        delete p;
+        return st;
+    }
+    if (cudaMalloc(&p->d_allkeys, sizeof(int64_t) * 2 * W * nranks) != cudaSuccess ||
+        cudaMalloc(&p->d_allexp, sizeof(int32_t) * 2 * W * nranks) != cudaSuccess ||
+        cudaMalloc(&p->d_alln, sizeof(int32_t) * nranks) != cudaSuccess) {
+        delete p;
+        return CCL_OUT_OF_MEMORY;
+    }
+    p->allkeys.resize(2 * (size_t)W * nranks);
+    p->allexp.resize(2 * (size_t)W * nranks);
+    p->nband.resize(nranks);
+    *plan_out = p;
+    return CCL_OK;
+}
 
-    Band b;
-    ccl_status st = band_init(b, band_H, W, row0);
-    if (st != CCL_OK) return st;
+ccl_status ccl_shard_plan_destroy(ccl_shard_plan p) {
+    if (!p) return CCL_INVALID_ARGUMENT;
+    delete p;
+    return CCL_OK;
+}
+
+ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32_t *band_labels,
+                                int32_t *n_components, ccl_stream_t stream) {
+    if (!p || !band_img || !band_labels || !n_components) return CCL_INVALID_ARGUMENT;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    Band &b = p->b;
+    const int W = p->W, nranks = p->nranks, rank = p->rank;
     // A + X1
-    st = band_phase_a(b, band_img, s);
+    ccl_status st = band_phase_a(b, band_img, s);
     if (st != CCL_OK) return st;
-    int64_t *d_allkeys = nullptr;
-    int32_t *d_allexp = nullptr, *d_alln = nullptr;
-    CK(cudaMalloc(&d_allkeys, sizeof(int64_t) * 2 * W * nranks));
-    CK(cudaMalloc(&d_allexp, sizeof(int32_t) * 2 * W * nranks));
-    CK(cudaMalloc(&d_alln, sizeof(int32_t) * nranks));
-    CKN(ncclAllGather(b.d_keys, d_allkeys, 2 * (size_t)W, ncclInt64, comm, s));
-    std::vector<int64_t> allkeys(2 * (size_t)W * nranks);
-    CK(cudaMemcpyAsync(allkeys.data(), d_allkeys, sizeof(int64_t) * allkeys.size(), cudaMemcpyDeviceToHost, s));
+    CKN(ncclAllGather(b.d_keys, p->d_allkeys, 2 * (size_t)W, ncclInt64, p->comm, s));
+    CK(cudaMemcpyAsync(p->allkeys.data(), p->d_allkeys, sizeof(int64_t) * p->allkeys.size(),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    memcpy(b.keys.data(), allkeys.data() + 2 * (size_t)W * rank, sizeof(int64_t) * 2 * W);
+    memcpy(b.keys.data(), p->allkeys.data() + 2 * (size_t)W * rank, sizeof(int64_t) * 2 * W);
     std::vector<const int64_t *> rows(2 * nranks);
     for (int k = 0; k < nranks; k++) {
-        rows[2 * k] = allkeys.data() + 2 * (size_t)W * k;
+        rows[2 * k] = p->allkeys.data() + 2 * (size_t)W * k;
         rows[2 * k + 1] = rows[2 * k] + W;
     }
     Resolver res;
     res.build(nranks, W, rows.data());
     // B + C + X2
-    st = band_phase_b(b, res, r0, bh, rank, s);
+    st = band_phase_b(b, res, {}, {}, rank, s);
     if (st == CCL_OK) st = band_phase_c(b, s);
     if (st != CCL_OK) return st;
-    CKN(ncclAllGather(b.d_small, d_alln, 1, ncclInt32, comm, s));
-    std::vector<int32_t> nband(nranks);
-    CK(cudaMemcpyAsync(nband.data(), d_alln, sizeof(int32_t) * nranks, cudaMemcpyDeviceToHost, s));
+    CKN(ncclAllGather(b.d_small, p->d_alln, 1, ncclInt32, p->comm, s));
+    CK(cudaMemcpyAsync(p->nband.data(), p->d_alln, sizeof(int32_t) * nranks, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int32_t off = 0, total = 0;
     for (int k = 0; k < nranks; k++) {
-        if (k < rank) off += nband[k];
-        total += nband[k];
+        if (k < rank) off += p->nband[k];
+        total += p->nband[k];
     }
     // D + X3
     st = band_phase_d(b, off, s);
     if (st != CCL_OK) return st;
-    CKN(ncclAllGather(b.d_exp, d_allexp, 2 * (size_t)W, ncclInt32, comm, s));
-    std::vector<int32_t> allexp(2 * (size_t)W * nranks);
-    CK(cudaMemcpyAsync(allexp.data(), d_allexp, sizeof(int32_t) * allexp.size(), cudaMemcpyDeviceToHost, s));
+    CKN(ncclAllGather(b.d_exp, p->d_allexp, 2 * (size_t)W, ncclInt32, p->comm, s));
+    CK(cudaMemcpyAsync(p->allexp.data(), p->d_allexp, sizeof(int32_t) * p->allexp.size(),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     std::vector<const int64_t *> akeys(nranks);
     std::vector<const int32_t *> aexp(nranks);
     for (int k = 0; k < nranks; k++) {
-        akeys[k] = allkeys.data() + 2 * (size_t)W * k;
-        aexp[k] = allexp.data() + 2 * (size_t)W * k;
+        akeys[k] = p->allkeys.data() + 2 * (size_t)W * k;
+        aexp[k] = p->allexp.data() + 2 * (size_t)W * k;
     }
     // E
     st = band_phase_e(b, akeys.data(), aexp.data(), nranks, band_labels, s);
     if (st != CCL_OK) return st;
-    CK(cudaMemcpyAsync(n_components, &total, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    p->total = total;
+    CK(cudaMemcpyAsync(n_components, &p->total, sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
-    cudaFree(d_allkeys);
-    cudaFree(d_allexp);
-    cudaFree(d_alln);
     return CCL_OK;
+}
+
+ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0, int H_total,
+                             int32_t *band_labels, int32_t *n_components, ccl_nccl_comm_t comm,
+                             ccl_stream_t stream) {
+    if (!band_img || !band_labels || !n_components) return CCL_INVALID_ARGUMENT;
+    ccl_shard_plan p = nullptr;
+    ccl_status st = ccl_shard_plan_create(band_H, W, row0, H_total, comm, stream, &p);
+    if (st != CCL_OK) return st;
+    st = ccl_shard_plan_label(p, band_img, band_labels, n_components, stream);
+    ccl_shard_plan_destroy(p);
+    return st;
 }
 
 }  // extern "C"

@@ -56,3 +56,23 @@ def test_full_c4_banded(nb):
     lo, no = oracle.label(img)
     lb, n = banded(img, nb)
     assert n == no and np.array_equal(lb, lo)
+
+
+def test_nccl_sharded_single_rank():
+    """The NCCL entry point end to end with a one-rank communicator (the
+    all-gathers run through NCCL; multi-rank runs need several GPUs)."""
+    img = synth.scaled("c4_voronoi_21600", 300, 2100)
+    uid = ccl.nccl_unique_id()
+    comm = ccl.NcclComm(uid, 1, 0)
+    t = torch.from_numpy(img).cuda()
+    lab, n = ccl.label_sharded(t, 0, img.shape[0], comm)
+    torch.cuda.synchronize()
+    lo, no = oracle.label(img)
+    assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo)
+    plan = ccl.ShardPlan(img.shape[0], img.shape[1], 0, img.shape[0], comm)
+    for _ in range(3):
+        lab, n = plan.label(t)
+        torch.cuda.synchronize()
+        assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo)
+    plan.close()
+    comm.close()
