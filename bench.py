@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 METRIC = "8-conn CCL Gpixel/s on 21600² image at 1/2/4/8 B200; % of HBM roofline"
 WORKLOAD = "c4_voronoi_21600"
 # algorithmic bytes per pixel: 1 B image read + 4 B label write
-ALG_BYTES_PER_PX = {"path": 5, "k_pack": 1, "k_tile_local": 0, "k_write": 4,
+ALG_BYTES_PER_PX = {"path": 5, "k_pack": 1, "k_fill": 0, "k_tile_local": 0, "k_write": 4,
                     "k_border": 0, "k_roots": 0, "k_scan": 0, "k_final": 0}
 
 
@@ -207,7 +207,7 @@ def main():
         step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
         nTx, nTy = (W + 1023) // 1024, (H + 31) // 32
         # mirrors cclb::pipeline_launches: k_border only runs when tiles have neighbours
-        launches_per_step = 6 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
+        launches_per_step = 7 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
     else:
         uid = ccl.nccl_unique_id() if rank == 0 else None
         obj = [uid]

@@ -27,7 +27,7 @@ Geometry make_geometry(int H, int W) {
 }
 
 enum {
-    A_BM, A_RUNCOMP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODESEG,
+    A_BM, A_FM, A_RUNCOMP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODESEG,
     A_GNODERANK, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE,
     A_TICKET, A_COUNT
 };
@@ -36,6 +36,7 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
     const size_t nT = (size_t)g.nT, H = (size_t)g.H;
     const size_t sz[A_COUNT] = {
         H * g.WW * 4,                   // bm
+        H * g.WW * 4,                   // fm
         H * g.nTx * MAXRUN * 2,         // runcomp
         nT * CAPC * 4,                  // compkey
         nT * CAPC * 4,                  // compnode
@@ -69,6 +70,7 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     char *b = static_cast<char *>(base);
     Workspace w;
     w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
+    w.fm = reinterpret_cast<uint32_t *>(b + offs[A_FM]);
     w.runcomp = reinterpret_cast<uint16_t *>(b + offs[A_RUNCOMP]);
     w.compkey = reinterpret_cast<int32_t *>(b + offs[A_COMPKEY]);
     w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);

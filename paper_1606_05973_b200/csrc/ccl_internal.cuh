@@ -39,6 +39,7 @@ struct Geometry {
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
+    uint32_t *fm;         // [H][WW]           bm with bridged single-pixel holes set (run mask)
     uint16_t *runcomp;    // [H][nTx][MAXRUN]  tile component of each run of each tile row
     int32_t *compkey;     // [nT][CAPC]        (row << 16 | run ordinal) of the component's root run
     int32_t *compnode;    // [nT][CAPC]        border-node id, or -1 (component inside the tile)
@@ -68,7 +69,7 @@ Geometry make_geometry(int H, int W);
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 
-enum { K_PACK = 0, K_TILE, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
+enum { K_PACK = 0, K_FILL, K_TILE, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it

@@ -31,8 +31,8 @@ namespace cclb {
 
 #define FULL 0xFFFFFFFFu
 
-const char *const kKernelNames[K_COUNT] = {"k_pack", "k_tile_local", "k_border", "k_roots",
-                                           "k_scan", "k_final", "k_write"};
+const char *const kKernelNames[K_COUNT] = {"k_pack", "k_fill", "k_tile_local", "k_border",
+                                           "k_roots", "k_scan", "k_final", "k_write"};
 
 // ===================================================================== helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -261,6 +261,29 @@ k_pack(const uint8_t *__restrict__ img, Geometry g, uint32_t *__restrict__ bm) {
     __stcg(bm + i, load_word(img, g, row, 32 * word));
 }
 
+// ======================================================================== K0b
+// Bridged single-pixel holes: a background pixel whose left and right
+// neighbours are foreground and whose pixel directly above or below is
+// foreground is set in fm (the run mask K1, K2 and K5 work on).  Both sides
+// of such a hole already touch that upper/lower pixel, so the partition of
+// the real foreground pixels is unchanged, and a filled pixel is never a run
+// head or a component's first pixel (its left neighbour precedes it).  On
+// images with isolated holes this halves the runs.  K5 still
+// writes 0 on filled pixels: it tests foreground on bm.
+__global__ void __launch_bounds__(256)
+k_fill(Geometry g, const uint32_t *__restrict__ bm, uint32_t *__restrict__ fm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)g.H * g.WW) return;
+    const int row = (int)(i / g.WW), word = (int)(i % g.WW);
+    const uint32_t x = __ldcg(bm + i);
+    const uint32_t xl = word > 0 ? __ldcg(bm + i - 1) : 0u;
+    const uint32_t xr = word + 1 < g.WW ? __ldcg(bm + i + 1) : 0u;
+    const uint32_t u = row > 0 ? __ldcg(bm + i - g.WW) : 0u;
+    const uint32_t d = row + 1 < g.H ? __ldcg(bm + i + g.WW) : 0u;
+    const uint32_t holes = ~x & ((x << 1) | (xl >> 31)) & ((x >> 1) | (xr << 31));
+    __stcg(fm + i, x | (holes & (u | d)));
+}
+
 // ========================================================================= K1
 // Tile-local two-pass labeling with runs as the provisional labels.  A run's
 // index k (row-major over the tile) plays the role of ARemSP's provisional
@@ -346,7 +369,7 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
         uint32_t xs[S];
 #pragma unroll
         for (int i = 0; i < S; i++)
-            xs[i] = (r0 + i < rows && gword < g.WW) ? __ldcg(ws.bm + (int64_t)(R0 + r0 + i) * g.WW + gword) : 0u;
+            xs[i] = (r0 + i < rows && gword < g.WW) ? __ldcg(ws.fm + (int64_t)(R0 + r0 + i) * g.WW + gword) : 0u;
 #pragma unroll
         for (int i = 0; i < S; i++) {
             const int rl = r0 + i;
@@ -587,8 +610,8 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
         const int ru = ty * TH - 1, rx = ty * TH;
         const int gword = tx * WPR + lane;
-        const uint32_t u = gword < g.WW ? ws.bm[(int64_t)ru * g.WW + gword] : 0u;
-        const uint32_t x = gword < g.WW ? ws.bm[(int64_t)rx * g.WW + gword] : 0u;
+        const uint32_t u = gword < g.WW ? ws.fm[(int64_t)ru * g.WW + gword] : 0u;
+        const uint32_t x = gword < g.WW ? ws.fm[(int64_t)rx * g.WW + gword] : 0u;
         RowView U = make_row(u), X = make_row(x);
         shd[wib][0][lane] = U.hx; sbs[wib][0][lane] = U.base;
         shd[wib][1][lane] = X.hx; sbs[wib][1][lane] = X.base;
@@ -612,7 +635,7 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             const uint32_t s = smear_up(t, x);
             const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
             const uint32_t S_ = s | (cin ? (x & ~(x + 1)) : 0u);
-            const uint32_t d = gword < g.WW ? ws.bm[(int64_t)(ru - 1) * g.WW + gword] : 0u;
+            const uint32_t d = gword < g.WW ? ws.fm[(int64_t)(ru - 1) * g.WW + gword] : 0u;
             m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_) & ~hole_bridged(u, U.xp, d);
         }
         while (m) {
@@ -832,9 +855,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
-    const uint32_t x = gword < g.WW ? __ldcs(ws.bm + (int64_t)row * g.WW + gword) : 0u;
-    const uint32_t xl = __shfl_up_sync(FULL, x, 1);
-    const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
+    const uint32_t f = gword < g.WW ? __ldcg(ws.fm + (int64_t)row * g.WW + gword) : 0u;  // runs
+    const uint32_t x = gword < g.WW ? __ldcg(ws.bm + (int64_t)row * g.WW + gword) : 0u;  // foreground
+    const uint32_t fl = __shfl_up_sync(FULL, f, 1);
+    const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     int32_t *rowlab = s_lab[wi];
@@ -884,9 +908,10 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     if (tx >= g.nTx) return;
     const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int gword = tx * WPR + lane;
+    const uint32_t f = gword < g.WW ? ws.fm[(int64_t)row * g.WW + gword] : 0u;
     const uint32_t x = gword < g.WW ? ws.bm[(int64_t)row * g.WW + gword] : 0u;
-    const uint32_t xl = __shfl_up_sync(FULL, x, 1);
-    const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
+    const uint32_t fl = __shfl_up_sync(FULL, f, 1);
+    const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * MAXRUN;
@@ -925,7 +950,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 6 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+    return 7 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
 static cudaError_t set_attrs() {
@@ -947,6 +972,8 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     {
         const int64_t words = (int64_t)g.H * g.WW;
         k_pack<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(img, g, ws.bm);
+        mark(K_FILL);
+        k_fill<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(g, ws.bm, ws.fm);
     }
     mark(K_TILE);
     k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(g, ws, g_k1_stop, g_k1_exper);

@@ -133,7 +133,7 @@ def test_kernel_times_profiling():
     plan.set_profiling(1)
     plan.label(img)
     t = plan.kernel_times()
-    assert set(t) == {"k_pack", "k_tile_local", "k_border", "k_roots", "k_scan", "k_final", "k_write"}
+    assert set(t) == {"k_pack", "k_fill", "k_tile_local", "k_border", "k_roots", "k_scan", "k_final", "k_write"}
     assert all(v >= 0 for v in t.values())
 
 
