@@ -20,16 +20,18 @@ Geometry make_geometry(int H, int W) {
     g.nTy = (H + TH - 1) / TH;
     g.nT = g.nTx * g.nTy;
     g.nseg = H * g.nTx;
-    g.nscan = (g.nseg + SCAN_TILE - 1) / SCAN_TILE;
+    const int tw = W < TW ? W : TW, th = H < TH ? H : TH;
+    g.maxrun = (tw + 1) / 2;
+    g.capc = ((th + 1) / 2) * g.maxrun;
+    g.capb = 2 * g.maxrun + th;
     g.aligned = (W % 16) == 0;
     g.row0 = 0;
     return g;
 }
 
 enum {
-    A_BM, A_FM, A_RUNCOMP, A_COMPKEY, A_COMPNODE, A_COMPRANK, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODESEG,
-    A_GNODERANK, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE,
-    A_TICKET, A_COUNT
+    A_BM, A_FM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
+    A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_COUNT
 };
 
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
@@ -37,23 +39,21 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
     const size_t sz[A_COUNT] = {
         H * g.WW * 4,                   // bm
         H * g.WW * 4,                   // fm
-        H * g.nTx * MAXRUN * 2,         // runcomp
-        nT * CAPC * 4,                  // compkey
-        nT * CAPC * 4,                  // compnode
-        nT * CAPC * 4,                  // comprank
-        nT * CAPC * 4,                  // complab
-        nT * CAPB * 4,                  // gparent
-        nT * CAPB * 8,                  // gkey
-        nT * CAPB * 4,                  // gnodeseg
-        nT * CAPB * 4,                  // gnoderank
-        nT * MAXRUN * 4,                // topnode
-        nT * MAXRUN * 4,                // botnode
+        H * g.nTx * g.maxrun * 2,       // runcomp
+        nT * g.capc * 4,                // compnode
+        nT * g.capc * 4,                // complab
+        nT * g.capb * 4,                // gparent
+        nT * g.capb * 8,                // gkey
+        nT * g.capb * 4,                // gnodecomp
+        nT * g.capb * 4,                // gnodelab
+        nT * g.maxrun * 4,              // topnode
+        nT * g.maxrun * 4,              // botnode
         (size_t)g.nTx * H * 4,          // leftnode
         (size_t)g.nTx * H * 4,          // rightnode
         nT * META * 4,                  // meta
         (size_t)g.nseg * 4,             // segcnt
         (size_t)g.nseg * 4,             // segoff
-        (size_t)g.nscan * 8,            // scanstate
+        (size_t)g.nTy * 8,              // scanstate
         16,                             // ticket
     };
     size_t o = 0;
@@ -72,14 +72,12 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
     w.fm = reinterpret_cast<uint32_t *>(b + offs[A_FM]);
     w.runcomp = reinterpret_cast<uint16_t *>(b + offs[A_RUNCOMP]);
-    w.compkey = reinterpret_cast<int32_t *>(b + offs[A_COMPKEY]);
     w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);
-    w.comprank = reinterpret_cast<uint32_t *>(b + offs[A_COMPRANK]);
     w.complab = reinterpret_cast<int32_t *>(b + offs[A_COMPLAB]);
     w.gparent = reinterpret_cast<int32_t *>(b + offs[A_GPARENT]);
     w.gkey = reinterpret_cast<int64_t *>(b + offs[A_GKEY]);
-    w.gnodeseg = reinterpret_cast<int32_t *>(b + offs[A_GNODESEG]);
-    w.gnoderank = reinterpret_cast<int32_t *>(b + offs[A_GNODERANK]);
+    w.gnodecomp = reinterpret_cast<int32_t *>(b + offs[A_GNODECOMP]);
+    w.gnodelab = reinterpret_cast<int32_t *>(b + offs[A_GNODELAB]);
     w.topnode = reinterpret_cast<int32_t *>(b + offs[A_TOP]);
     w.botnode = reinterpret_cast<int32_t *>(b + offs[A_BOT]);
     w.leftnode = reinterpret_cast<int32_t *>(b + offs[A_LEFT]);
@@ -89,7 +87,6 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.segoff = reinterpret_cast<int32_t *>(b + offs[A_SEGOFF]);
     w.scanstate = reinterpret_cast<unsigned long long *>(b + offs[A_SCANSTATE]);
     w.ticket = reinterpret_cast<int32_t *>(b + offs[A_TICKET]);
-    w.boff = nullptr;
     w.xlab = nullptr;
     return w;
 }

@@ -97,7 +97,7 @@ struct Band {
     int64_t *d_keys = nullptr;  // 2 * W
     int32_t *d_nodes = nullptr; // 2 * W
     int32_t *d_exp = nullptr;   // 2 * W
-    int32_t *d_small = nullptr; // [0] N_band, [1] band offset
+    int32_t *d_small = nullptr; // [0] N_band
     int32_t *d_xlab = nullptr;  // foreign labels
     int2 *d_act = nullptr;      // re-links
     size_t xlab_cap = 0, act_cap = 0;
@@ -106,6 +106,7 @@ struct Band {
     std::vector<int32_t> nodes;  // 2 * W
     std::vector<int64_t> fkeys;  // foreign class minima (index f -> key)
     int band_H = 0, row0 = 0;
+    int32_t offset = 0;          // labels of earlier bands (phase D)
 
     ~Band() { release(); }
     void release() {
@@ -150,7 +151,6 @@ ccl_status band_init(Band &b, int band_H, int W, int row0) {
     CK(cudaMalloc(&b.d_nodes, sizeof(int32_t) * 2 * W));
     CK(cudaMalloc(&b.d_exp, sizeof(int32_t) * 2 * W));
     CK(cudaMalloc(&b.d_small, sizeof(int32_t) * 4));
-    b.ws.boff = b.d_small + 1;
     b.keys.resize(2 * (size_t)W);
     b.nodes.resize(2 * (size_t)W);
     return CCL_OK;
@@ -224,13 +224,12 @@ ccl_status band_phase_c(Band &b, cudaStream_t s) {
     return CCL_OK;
 }
 
-// D: with the band offset in d_small[1], the labels of the boundary-row roots
+// D: with the band offset, the labels of the boundary-row roots
 ccl_status band_phase_d(Band &b, int32_t offset, cudaStream_t s) {
     const int W = b.g.W;
-    CK(cudaMemcpyAsync(b.d_small + 1, &offset, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(band_export(b.g, b.ws, b.d_nodes, b.d_exp, s));
-    CK(band_export(b.g, b.ws, b.d_nodes + W, b.d_exp + W, s));
-    CK(cudaStreamSynchronize(s));  // offset is a host temporary
+    b.offset = offset;
+    CK(band_export(b.g, b.ws, b.d_nodes, b.d_exp, offset, s));
+    CK(band_export(b.g, b.ws, b.d_nodes + W, b.d_exp + W, offset, s));
     return CCL_OK;
 }
 
@@ -257,7 +256,7 @@ ccl_status band_phase_e(Band &b, const int64_t *const *all_keys, const int32_t *
         CK(cudaMemcpyAsync(b.d_xlab, xl.data(), sizeof(int32_t) * xl.size(), cudaMemcpyHostToDevice, s));
     }
     b.ws.xlab = b.d_xlab;
-    CK(run_stage_final(b.g, b.ws, labels, s, nullptr));
+    CK(run_stage_final(b.g, b.ws, labels, b.offset, s, nullptr));
     CK(cudaStreamSynchronize(s));  // xl is a host temporary
     return CCL_OK;
 }

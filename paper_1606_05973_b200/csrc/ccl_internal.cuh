@@ -12,18 +12,18 @@ constexpr int WPR = TW / 32;           // 32-bit words per tile row
 constexpr int NW = 8;                  // warps per K1 CTA
 constexpr int S = 4;                   // rows per warp in K1
 constexpr int TH = NW * S;             // tile height (32)
-constexpr int MAXRUN = TW / 2;         // max runs in one tile row
+constexpr int MAXRUN = TW / 2;         // max runs in one tile row (smem bound)
 constexpr int RCAP = TH * MAXRUN;      // max runs in one tile (16384 < 2^15)
 // Components of a tile are at most its largest set of pairwise non-adjacent
-// pixels (king's graph): ceil(TH/2) * ceil(TW/2).
+// pixels (king's graph): ceil(TH/2) * ceil(TW/2).  Geometry::capc is the same
+// bound for the actual tile width (narrow images get small workspaces).
 constexpr int CAPC = (TH / 2) * (TW / 2);
-constexpr int CAPB = 2 * MAXRUN + TH;  // components touching the tile border
-constexpr int META = 4;                // ints of per-tile metadata
+constexpr int META = 40;               // ints of per-tile metadata
 constexpr int META_NCOMP = 0, META_NBORDER = 1, META_ROWS = 2;
+constexpr int META_ROWFIRST = 4;       // [TH+1] first component index of each tile row
 
-constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_ITEMS = 16;
-constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int KN_WARPS = 8;            // k_number: warps per tile-row CTA
+constexpr int KN_ITEMS = 4;            // k_number: segments per thread per scan chunk
 
 struct Geometry {
     int H, W;
@@ -31,7 +31,9 @@ struct Geometry {
     int nTx, nTy;  // tile grid
     int nT;        // nTx * nTy
     int nseg;      // H * nTx: (row, tile-column) segments in raster order
-    int nscan;     // decoupled-lookback partitions over the segments
+    int maxrun;    // runs per tile row bound: ceil(min(W,TW)/2)
+    int capc;      // components per tile bound: ceil(min(H,TH)/2) * maxrun
+    int capb;      // border components per tile bound: 2*maxrun + min(H,TH)
     int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
     int row0;      // global row of this image's row 0 (row bands of a sharded image; else 0)
 };
@@ -40,26 +42,23 @@ struct Geometry {
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
     uint32_t *fm;         // [H][WW]           bm with bridged single-pixel holes set (run mask)
-    uint16_t *runcomp;    // [H][nTx][MAXRUN]  tile component of each run of each tile row
-    int32_t *compkey;     // [nT][CAPC]        (row << 16 | run ordinal) of the component's root run
-    int32_t *compnode;    // [nT][CAPC]        border-node id, or -1 (component inside the tile)
-    uint32_t *comprank;   // [nT][CAPC]        (row<<16 | rank within its segment) for global roots
-    int32_t *complab;     // [nT][CAPC]        final label of the component
-    int32_t *gparent;     // [nT][CAPB]        global union-find over border components
-    int64_t *gkey;        // [nT][CAPB]        (image row, tile column, run ordinal) key: raster order
-    int32_t *gnodeseg;    // [nT][CAPB]        segment of a root node's first pixel
-    int32_t *gnoderank;   // [nT][CAPB]        rank of a root node inside that segment
-    int32_t *topnode;     // [nT][MAXRUN]      node of each run of the tile's first row
-    int32_t *botnode;     // [nT][MAXRUN]      node of each run of the tile's last row
+    uint16_t *runcomp;    // [H][nTx][maxrun]  tile component of each run of each tile row
+    int32_t *compnode;    // [nT][capc]        border-node id of a border component (others unset)
+    int32_t *complab;     // [nT][capc]        band-local label of the component (1..N_band)
+    int32_t *gparent;     // [nT][capb]        global union-find over border components
+    int64_t *gkey;        // [nT][capb]        (image row, tile column, run ordinal) key: raster order
+    int32_t *gnodecomp;   // [nT][capb]        (root row in tile << 16) | tile component of the node
+    int32_t *gnodelab;    // [nT][capb]        band-local label of a root node
+    int32_t *topnode;     // [nT][maxrun]      node of each run of the tile's first row
+    int32_t *botnode;     // [nT][maxrun]      node of each run of the tile's last row
     int32_t *leftnode;    // [nTx][H]          node of the pixel in the tile's first column
     int32_t *rightnode;   // [nTx][H]          node of the pixel in the tile's last column
-    int32_t *meta;        // [nT][META]
+    int32_t *meta;        // [nT][META]        ncomp, nborder, rows, rowfirst[TH+1]
     int32_t *segcnt;      // [nseg]            global roots whose first pixel lies in the segment
-    int32_t *segoff;      // [nseg]            exclusive prefix of segcnt (raster order)
-    unsigned long long *scanstate;  // [nscan] decoupled-lookback descriptors
+    int32_t *segoff;      // [nseg]            exclusive prefix of segcnt inside its tile row
+    unsigned long long *scanstate;  // [nTy]   decoupled-lookback descriptors (one per tile row)
     int32_t *ticket;      // [1]               dynamic partition counter
     // row bands only (null for a whole image):
-    const int32_t *boff;  // [1]               labels of earlier bands (added to every label)
     const int32_t *xlab;  // [*]               labels of roots owned by other bands; a node
                           //                   whose parent is -2-f takes xlab[f]
 };
@@ -69,7 +68,7 @@ Geometry make_geometry(int H, int W);
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 
-enum { K_PACK = 0, K_FILL, K_TILE, K_BORDER, K_ROOTS, K_SCAN, K_FINAL, K_WRITE, K_COUNT };
+enum { K_TILE = 0, K_BORDER, K_NUMBER, K_FIXUP, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it
@@ -78,14 +77,16 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev);
 // The same pipeline in three stages (row bands insert the cross-band step
-// between them): local = pack, tile labeling, tile-edge merge;
-// count = roots + numbering scan (N of this image/band -> *n_components);
-// final = component labels + label write.
+// between them): local = tile labeling (incl. the foreground predicate) +
+// tile-edge merge; count = roots, numbering scan and labels of the roots (N of
+// this image/band -> *n_components); final = labels of merged components +
+// label write.
 cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
                             cudaStream_t stream, cudaEvent_t *ev);
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev);
-cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+// boff = labels of earlier row bands (0 for a whole image), added to every label.
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels, int32_t boff,
                             cudaStream_t stream, cudaEvent_t *ev);
 // Row bands: per-pixel root key / root node of local row `row` (-1 background).
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
@@ -95,7 +96,7 @@ cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t
 // Per pixel of local row `row`: the final label if the pixel's root node (from
 // band_row_roots) is still a root after band_apply, else -1.
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
-                        int32_t *labels_out, cudaStream_t stream);
+                        int32_t *labels_out, int32_t boff, cudaStream_t stream);
 // Number of kernel launches run_pipeline makes for this geometry.
 int pipeline_launches(const Geometry &g);
 

@@ -1,24 +1,27 @@
 // ccl_kernels.cu -- B200 (sm_100a) kernels of the two-pass 8-connectivity CCL
 // pipeline.  DESIGN.md explains the design; paper citations are PAPER.md lines.
 //
-//   K0 k_pack         image -> 1 bit per pixel (128-bit streaming loads).
-//   K1 k_tile_local   one CTA per 32x1024 tile of row masks; the runs of the tile
-//                     are its provisional labels (index order = raster order).
-//                     Scan: every run copies its leftmost upper neighbour's
-//                     label (Scan_ARemSP's copy), 8 strips
-//                     at once; a short find resolves the copies;
-//                     the few remaining edges merged with a lock-free Rem's
-//                     union with splicing (merge / merger, PAPER.md:669-698,
-//                     1001-1046); roots numbered in raster order.
+//   K1 k_tile_local   one CTA per 32x1024 image tile: reads the pixels once
+//                     (16-byte streaming loads; fg = byte != 0),
+//                     packs them to row masks and fills bridged single-pixel
+//                     holes; the runs of the tile are its provisional labels
+//                     (index order = raster order).  Scan: every run copies its
+//                     leftmost upper neighbour's label (Scan_ARemSP's copy,
+//                     PAPER.md:871-892), 8 strips at once; a short find resolves
+//                     the copies; the few remaining edges are
+//                     merged with a lock-free Rem's union with splicing (merge /
+//                     merger); roots numbered in
+//                     raster order.
 //   K2 k_border       lock-free atomicCAS union of the components that touch
 //                     across tile edges (PARemSP's boundary merge, PAPER.md:971-988,
 //                     with CAS in place of omp locks).
-//   K3 k_roots        per tile: which components are global roots, and their
-//                     rank inside their (row, tile-column) segment.
-//   K4 k_scan         hand-written decoupled-lookback exclusive scan of the
-//                     per-segment root counts = flatten's consecutive numbering
-//                     k++  in raster order; writes N.
-//   K4b k_final       final label of every tile component.
+//   K3 k_number       one CTA per tile row: which components are global roots,
+//                     root counts per (row, tile-column) segment, a hand-written
+//                     decoupled-lookback scan over the tile rows = flatten's
+//                     consecutive numbering k++  in raster
+//                     order; labels of all roots; writes N.
+//   K4 k_fixup        labels of the border components that are not global roots
+//                     (their root's label).
 //   K5 k_write        labeling phase: every pixel gets its
 //                     component's label; coalesced 16-byte streaming stores.
 #include <cuda_runtime.h>
@@ -31,8 +34,8 @@ namespace cclb {
 
 #define FULL 0xFFFFFFFFu
 
-const char *const kKernelNames[K_COUNT] = {"k_pack", "k_fill", "k_tile_local", "k_border",
-                                           "k_roots", "k_scan", "k_final", "k_write"};
+const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number", "k_fixup",
+                                           "k_write"};
 
 // ===================================================================== helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -208,11 +211,6 @@ __device__ __forceinline__ int gfind_ro(const int32_t *par, int x) {
         x = px;
     }
 }
-// Final label of a root node (or a foreign reference).
-__device__ __forceinline__ int32_t node_label(const Workspace &ws, int root, int32_t off) {
-    if (root < 0) return ws.xlab[-2 - root];
-    return off + ws.segoff[ws.gnodeseg[root]] + ws.gnoderank[root] + 1;
-}
 // Links the root with the larger key under the root with the smaller key.
 __device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
     while (true) {
@@ -224,13 +222,27 @@ __device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
     }
 }
 
+// 8 bytes of pixels (words a, b) -> 8 bits, bit k = (byte k != 0).  Bit 7 of
+// every byte of f is its "nonzero" flag; the flags of a go to bit 0 and those
+// of b to bit 4 of each byte, and one multiply gathers bit 8j -> 24+j and
+// 8j+4 -> 28+j (the partial products never overlap, so nothing carries).
+__device__ __forceinline__ uint32_t pack8(uint32_t a, uint32_t b) {
+    const uint32_t fa = ((a & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | a;
+    const uint32_t fb = ((b & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | b;
+    const uint32_t v = ((fa >> 7) & 0x01010101u) | ((fb >> 3) & 0x10101010u);
+    return (v * 0x01020408u) >> 24;
+}
 // 16 bytes of pixels -> 16 bits (bit k = byte k != 0)
 __device__ __forceinline__ uint32_t pack16(uint4 v) {
-    auto nz4 = [](uint32_t w) -> uint32_t {
-        uint32_t m = (((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u;
-        return ((m >> 7) * 0x01020408u) >> 24;
-    };
-    return nz4(v.x) | (nz4(v.y) << 4) | (nz4(v.z) << 8) | (nz4(v.w) << 12);
+    return pack8(v.x, v.y) | (pack8(v.z, v.w) << 8);
+}
+
+// Rows whose length is not a multiple of 16 bytes: byte loads (kept out of line).
+__device__ __noinline__ uint32_t load_word_bytes(const uint8_t *src, int n) {
+    uint32_t m = 0;
+#pragma unroll 1
+    for (int i = 0; i < n; i++) m |= (uint32_t)(__ldcs(src + i) != 0) << i;
+    return m;
 }
 
 // Load the 32 pixels of lane-word (row, word) as a bitmask.
@@ -243,45 +255,7 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
         if (col0 + 16 < g.W) m |= pack16(__ldcs(reinterpret_cast<const uint4 *>(src + 16))) << 16;
         return m;
     }
-    uint32_t m = 0;
-    int n = min(32, g.W - col0);
-    for (int i = 0; i < n; i++) m |= (uint32_t)(__ldcs(src + i) != 0) << i;
-    return m;
-}
-
-// ========================================================================= K0
-// Foreground predicate (reading A10: byte != 0), packed to
-// one bit per pixel: thread = one 32-pixel word of the bitmask.  Streaming,
-// bandwidth-bound: the image is read exactly once here.
-__global__ void __launch_bounds__(256)
-k_pack(const uint8_t *__restrict__ img, Geometry g, uint32_t *__restrict__ bm) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)g.H * g.WW) return;
-    const int row = (int)(i / g.WW), word = (int)(i % g.WW);
-    __stcg(bm + i, load_word(img, g, row, 32 * word));
-}
-
-// ======================================================================== K0b
-// Bridged single-pixel holes: a background pixel whose left and right
-// neighbours are foreground and whose pixel directly above or below is
-// foreground is set in fm (the run mask K1, K2 and K5 work on).  Both sides
-// of such a hole already touch that upper/lower pixel, so the partition of
-// the real foreground pixels is unchanged, and a filled pixel is never a run
-// head or a component's first pixel (its left neighbour precedes it).  On
-// images with isolated holes this halves the runs.  K5 still
-// writes 0 on filled pixels: it tests foreground on bm.
-__global__ void __launch_bounds__(256)
-k_fill(Geometry g, const uint32_t *__restrict__ bm, uint32_t *__restrict__ fm) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)g.H * g.WW) return;
-    const int row = (int)(i / g.WW), word = (int)(i % g.WW);
-    const uint32_t x = __ldcg(bm + i);
-    const uint32_t xl = word > 0 ? __ldcg(bm + i - 1) : 0u;
-    const uint32_t xr = word + 1 < g.WW ? __ldcg(bm + i + 1) : 0u;
-    const uint32_t u = row > 0 ? __ldcg(bm + i - g.WW) : 0u;
-    const uint32_t d = row + 1 < g.H ? __ldcg(bm + i + g.WW) : 0u;
-    const uint32_t holes = ~x & ((x << 1) | (xl >> 31)) & ((x >> 1) | (xr << 31));
-    __stcg(fm + i, x | (holes & (u | d)));
+    return load_word_bytes(src, min(32, g.W - col0));
 }
 
 // ========================================================================= K1
@@ -297,6 +271,7 @@ struct K1Smem {
     uint16_t hbase[TH][WPR];       // runs whose head lies in earlier words of the row
     int32_t nrun[TH];              // runs per row
     int32_t rowbase[TH + 1];       // runs in earlier rows
+    int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t wscan[NW];             // block-scan scratch
 };
 
@@ -350,7 +325,7 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
 }
 
 __global__ void __launch_bounds__(NW * 32, 4)
-k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
+k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop, int exper) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
 
@@ -364,25 +339,49 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
     const int r0 = w * S;
     volatile uint16_t *vp = sm.p;
 
-    // ---- P0: row masks (from K0), run heads, per-word run counts
-    {
-        uint32_t xs[S];
+    if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
+        for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
+        if (threadIdx.x == 0) *ws.ticket = 0;
+    }
+    if (threadIdx.x < TH) sm.rowcnt[threadIdx.x] = 0;
+    // ---- P0: the pixels of the tile, read once with 16-byte streaming loads:
+    // fg = byte != 0 (reading A10), one bit per pixel.  The
+    // warp's S rows are all in flight before the first is used.
+    uint32_t xs[S];
 #pragma unroll
-        for (int i = 0; i < S; i++)
-            xs[i] = (r0 + i < rows && gword < g.WW) ? __ldcg(ws.fm + (int64_t)(R0 + r0 + i) * g.WW + gword) : 0u;
+    for (int i = 0; i < S; i++)
+        xs[i] = (r0 + i < rows && gword < g.WW) ? load_word(img, g, R0 + r0 + i, 32 * gword) : 0u;
 #pragma unroll
-        for (int i = 0; i < S; i++) {
-            const int rl = r0 + i;
-            const uint32_t x = xs[i];
-            const uint32_t xl = __shfl_up_sync(FULL, x, 1);
-            const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xl >> 31)));
-            uint32_t nr;
-            const uint32_t base = warp_excl_scan(__popc(hx), nr);
-            sm.bm[rl][lane] = x;
-            sm.hd[rl][lane] = hx;
-            sm.hbase[rl][lane] = (uint16_t)base;
-            if (lane == 0) sm.nrun[rl] = (int)nr;
-        }
+    for (int i = 0; i < S; i++) {
+        sm.mc[r0 + i][lane] = xs[i];  // raw masks (mc is free until P2a)
+        if (r0 + i < rows && gword < g.WW) ws.bm[(int64_t)(R0 + r0 + i) * g.WW + gword] = xs[i];
+    }
+    __syncthreads();
+    // ---- P0b: run mask = foreground + bridged single-pixel holes (a background
+    // pixel whose left and right neighbours and the pixel above or below are
+    // foreground).  Only holes whose neighbours lie in
+    // this tile are filled: any subset of bridged holes preserves the
+    // partition of the foreground, and K2/K5 read the same run mask.
+    // Then run heads and per-word run counts.
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i;
+        const uint32_t x0 = xs[i];
+        const uint32_t xlr = __shfl_up_sync(FULL, x0, 1), xrr = __shfl_down_sync(FULL, x0, 1);
+        const uint32_t xl = lane == 0 ? 0u : xlr, xr = lane == 31 ? 0u : xrr;
+        const uint32_t u = rl > 0 ? sm.mc[rl - 1][lane] : 0u;
+        const uint32_t d = rl + 1 < rows ? sm.mc[rl + 1][lane] : 0u;
+        const uint32_t holes = ~x0 & ((x0 << 1) | (xl >> 31)) & ((x0 >> 1) | (xr << 31));
+        const uint32_t x = x0 | (holes & (u | d));
+        if (rl < rows && gword < g.WW) ws.fm[(int64_t)(R0 + rl) * g.WW + gword] = x;
+        const uint32_t xfl = __shfl_up_sync(FULL, x, 1);
+        const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xfl >> 31)));
+        uint32_t nr;
+        const uint32_t base = warp_excl_scan(__popc(hx), nr);
+        sm.bm[rl][lane] = x;
+        sm.hd[rl][lane] = hx;
+        sm.hbase[rl][lane] = (uint16_t)base;
+        if (lane == 0) sm.nrun[rl] = (int)nr;
     }
     __syncthreads();
     if (w == 0) {
@@ -410,6 +409,7 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
             continue;
         }
         const int rb = sm.rowbase[rl], re = sm.rowbase[rl + 1];
+#pragma unroll 1
         for (int k = rb + lane; k < re; k += 32) vp[k] = (uint16_t)k;
         if (rl == 0) {
             sm.mc[rl][lane] = 0u;
@@ -505,23 +505,34 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
     }
     int ncomp;
     int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
-    // component key = (row, ordinal) of the root run's head: ordered like the
-    // raster index of the component's first pixel
-    int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
-    {
-        int rl = 0;  // row of run k0: the last row whose base is <= k0
+    // row of run k0: the last row whose base is <= k0
+    int rl0 = 0;
 #pragma unroll
-        for (int step = TH / 2; step > 0; step >>= 1)
-            if (sm.rowbase[rl + step] <= k0) rl += step;
+    for (int step = TH / 2; step > 0; step >>= 1)
+        if (sm.rowbase[rl0 + step] <= k0) rl0 += step;
+    {
+        int rl = rl0, run = 0;
         for (int k = k0; k < k1; k++) {
             if (sm.p[k] != (uint16_t)k) continue;
-            while (sm.rowbase[rl + 1] <= k) rl++;
-            compkey[cidx] = (rl << 16) | (k - sm.rowbase[rl]);
+            while (sm.rowbase[rl + 1] <= k) {
+                if (run) atomicAdd(&sm.rowcnt[rl], run);
+                run = 0;
+                rl++;
+            }
+            run++;
             sm.p[k] = (uint16_t)(0x8000 | cidx++);  // root: flag | component
         }
+        if (run) atomicAdd(&sm.rowcnt[rl], run);
     }
     __syncthreads();
     if (stop <= 3) return;
+    int32_t *meta = ws.meta + (int64_t)tile * META;
+    if (w == 0) {  // first component of every tile row (components are in key order)
+        uint32_t tot;
+        const int pre = (int)warp_excl_scan((uint32_t)sm.rowcnt[lane], tot);
+        meta[META_ROWFIRST + lane] = pre;
+        if (lane == 0) meta[META_ROWFIRST + TH] = (int)tot;
+    }
     auto comp_of = [&](int k) -> int {
         const uint32_t pk = sm.p[k];
         return (int)((pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu));
@@ -537,7 +548,8 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
         const int rl = r0 + i;
         if (rl >= rows) break;
         const int b = sm.rowbase[rl], n = sm.nrun[rl];
-        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * MAXRUN;
+        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
+#pragma unroll 1
         for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(b + o);
     }
     auto mark = [&](int k) {
@@ -558,21 +570,21 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
     for (int k = k0; k < k1; k++) bc += (sm.p[k] & 0xC000u) == 0xC000u;
     int nborder;
     int bidx = block_excl_scan(bc, sm.wscan, nborder);
-    int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
-    const int nodebase = tile * CAPB;
-    for (int k = k0; k < k1; k++) {
-        const uint32_t pk = sm.p[k];
-        if (!(pk & 0x8000u)) continue;
-        const int c = (int)(pk & 0x3FFFu);
-        if (pk & 0x4000u) {
+    int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
+    const int nodebase = tile * g.capb;
+    {
+        int rl = rl0;
+        for (int k = k0; k < k1; k++) {
+            const uint32_t pk = sm.p[k];
+            if ((pk & 0xC000u) != 0xC000u) continue;
+            while (sm.rowbase[rl + 1] <= k) rl++;
+            const int c = (int)(pk & 0x3FFFu);
             const int node = nodebase + bidx++;
-            const int key = compkey[c];
             compnode[c] = node;
             ws.gparent[node] = node;
+            ws.gnodecomp[node] = (rl << 16) | c;
             // global order = (image row, tile column, run ordinal): raster order
-            ws.gkey[node] = ((int64_t)(g.row0 + R0 + (key >> 16)) * g.nTx + tx) * MAXRUN + (key & 0xFFFF);
-        } else {
-            compnode[c] = -1;
+            ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + (k - sm.rowbase[rl]);
         }
     }
     __syncthreads();
@@ -580,8 +592,8 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
     // ---- P4c: nodes of the border pixels (for K2)
     {
         const int ntop = sm.nrun[0], bb = sm.rowbase[rows - 1], nbot = sm.nrun[rows - 1];
-        for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[tile * MAXRUN + o] = compnode[comp_of(o)];
-        for (int o = threadIdx.x; o < nbot; o += NW * 32) ws.botnode[tile * MAXRUN + o] = compnode[comp_of(bb + o)];
+        for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(o)];
+        for (int o = threadIdx.x; o < nbot; o += NW * 32) ws.botnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(bb + o)];
         for (int r = threadIdx.x; r < rows; r += NW * 32) {
             const int64_t off = (int64_t)tx * g.H + R0 + r;
             ws.leftnode[off] = (sm.bm[r][0] & 1u) ? compnode[comp_of(sm.rowbase[r])] : -1;
@@ -589,7 +601,6 @@ k_tile_local(Geometry g, Workspace ws, int stop, int exper) {
         }
     }
     if (threadIdx.x == 0) {
-        int32_t *meta = ws.meta + (int64_t)tile * META;
         meta[META_NCOMP] = ncomp;
         meta[META_NBORDER] = nborder;
         meta[META_ROWS] = rows;
@@ -616,8 +627,8 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         shd[wib][0][lane] = U.hx; sbs[wib][0][lane] = U.base;
         shd[wib][1][lane] = X.hx; sbs[wib][1][lane] = X.base;
         __syncwarp();
-        const int32_t *bot = ws.botnode + (int64_t)((ty - 1) * g.nTx + tx) * MAXRUN;
-        const int32_t *top = ws.topnode + (int64_t)(ty * g.nTx + tx) * MAXRUN;
+        const int32_t *bot = ws.botnode + (int64_t)((ty - 1) * g.nTx + tx) * g.maxrun;
+        const int32_t *top = ws.topnode + (int64_t)(ty * g.nTx + tx) * g.maxrun;
         uint32_t m = first_in_run(x & dilate(U), x);
         while (m) {
             int b = __ffs(m) - 1;
@@ -667,176 +678,207 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
 }
 
 // ========================================================================= K3
-// One warp per tile: component c is a global root iff it lies inside the
-// tile or its node is a root of the global forest (its key is the
-// component's minimum, i.e. its first pixel in raster order).  Counts roots
-// per (row, tile-column) segment and ranks each root inside its segment.
-constexpr int K3_WARPS = 8;
-__global__ void __launch_bounds__(K3_WARPS * 32)
-k_roots(Geometry g, Workspace ws) {
-    __shared__ int cnt[K3_WARPS][TH + 1];
-    const int lane = lane_id(), wi = threadIdx.x >> 5;
-    const int tile = blockIdx.x * K3_WARPS + wi;
-    if (blockIdx.x == 0) {  // reset the scan's lookback state for K4
-        for (int i = threadIdx.x; i < g.nscan; i += blockDim.x) ws.scanstate[i] = 0ull;
-        if (threadIdx.x == 0) *ws.ticket = 0;
-    }
-    if (tile >= g.nT) return;
-    const int tx = tile % g.nTx, ty = tile / g.nTx, R0 = ty * TH;
-    const int32_t *meta = ws.meta + (int64_t)tile * META;
-    const int ncomp = meta[META_NCOMP], rows = meta[META_ROWS];
-    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
-    const int32_t *compkey = ws.compkey + (int64_t)tile * CAPC;
-    uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
-    int *c_row = cnt[wi];
-    c_row[lane] = 0;
-    if (lane == 0) c_row[TH] = 0;
+// One CTA per tile row (32 image rows x all tile columns), claimed in raster
+// order through a ticket so that a CTA only ever waits on CTAs already running.
+// A component is a global root iff it lies inside its tile or its node is a
+// root of the global forest after K2 (its key is the component's minimum, i.e.
+// its first pixel in raster order).  Components of a tile are numbered in key
+// order (K1), so the roots of tile row r are the index range
+// [rowfirst[r], rowfirst[r+1]) minus the few border components that are not
+// roots.  The root counts of the tile row's segments (row, tile column) are
+// scanned in raster order, chained across tile rows with a decoupled
+// lookback, and every root gets  offset(segment) + rank in segment + 1:
+// flatten's consecutive numbering k++  made canonical.
+struct KNSmem {
+    uint32_t nrbits[KN_WARPS][CAPC / 32];  // non-root border components of the warp's tile
+    int32_t wpre[KN_WARPS][CAPC / 32];     // exclusive popcount prefix of nrbits
+    int32_t rowfirst[KN_WARPS][TH + 1];
+    int32_t nrrow[KN_WARPS][TH];           // non-roots per row, then their exclusive prefix
+    int32_t rbase[KN_WARPS][TH];           // label of the row's first root minus its index
+    int32_t wsum[KN_WARPS];
+    int32_t part, excl;
+};
+
+// Marks the tile's border components that are not roots in nrbits (and counts
+// them per row in nrrow); one warp.
+__device__ __forceinline__ void kn_nonroots(const Workspace &ws, int nodebase, int nborder,
+                                            uint32_t *bits, int nbw, int32_t *nrrow, bool setbits) {
+    const int lane = lane_id();
+    for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
+    nrrow[lane] = 0;
     __syncwarp();
-    // pass 1: roots per row
-    for (int c0 = 0; c0 < ncomp; c0 += 32) {
-        const int c = c0 + lane;
-        if (c < ncomp) {
-            const int node = compnode[c];
-            if (node < 0 || __ldcg(ws.gparent + node) == node) atomicAdd(&c_row[compkey[c] >> 16], 1);
+    for (int j = lane; j < nborder; j += 32) {
+        const int node = nodebase + j;
+        if (__ldcg(ws.gparent + node) != node) {
+            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
+            if (setbits) atomicOr(bits + (c >> 5), 1u << (c & 31));
+            atomicAdd(nrrow + (gc >> 16), 1);
         }
     }
     __syncwarp();
-    uint32_t tot;
-    const int rowstart = (int)warp_excl_scan((uint32_t)c_row[lane], tot);
-    const int mycnt = c_row[lane];
-    __syncwarp();
-    c_row[lane] = rowstart;
-    __syncwarp();
-    if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = mycnt;
-    // pass 2: rank = (roots before it in the tile) - (roots in earlier rows)
-    int run = 0;
-    for (int c0 = 0; c0 < ncomp; c0 += 32) {
-        const int c = c0 + lane;
-        bool root = false;
-        int node = -1, rl = 0;
-        if (c < ncomp) {
-            node = compnode[c];
-            root = node < 0 || __ldcg(ws.gparent + node) == node;
-            rl = compkey[c] >> 16;
+}
+
+__global__ void __launch_bounds__(KN_WARPS * 32, 4)
+k_number(Geometry g, Workspace ws, int32_t *n_components) {
+    __shared__ KNSmem sm;
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
+    __syncthreads();
+    const int ty = sm.part;
+    const int R0 = ty * TH, rows = min(TH, g.H - R0);
+    // ---- phase 1: root counts of the segments (R0 + r, tx)
+    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
+        const int tile = ty * g.nTx + tx;
+        const int32_t *meta = ws.meta + (int64_t)tile * META;
+        const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
+        kn_nonroots(ws, tile * g.capb, nborder, sm.nrbits[w], 0, sm.nrrow[w], false);
+        const int rf = __ldcg(meta + META_ROWFIRST + lane);
+        const int rfn = lane + 1 < rows ? __ldcg(meta + META_ROWFIRST + lane + 1) : ncomp;
+        if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = rfn - rf - sm.nrrow[w][lane];
+    }
+    __syncthreads();
+    // ---- phase 2: exclusive scan of the tile row's rows*nTx segment counts
+    // (raster order), then the lookback over earlier tile rows
+    const int64_t sbase = (int64_t)R0 * g.nTx;
+    const int nS = rows * g.nTx;
+    int carry = 0;
+    for (int c0 = 0; c0 < nS; c0 += KN_WARPS * 32 * KN_ITEMS) {
+        const int i0 = c0 + threadIdx.x * KN_ITEMS;
+        int v[KN_ITEMS], sum = 0;
+#pragma unroll
+        for (int i = 0; i < KN_ITEMS; i++) {
+            v[i] = i0 + i < nS ? __ldcg(ws.segcnt + sbase + i0 + i) : 0;
+            sum += v[i];
         }
-        const uint32_t bal = __ballot_sync(FULL, root);
-        if (c < ncomp) {
-            if (root) {
-                const int rk = run + __popc(bal & ((1u << lane) - 1)) - c_row[rl];
-                comprank[c] = ((uint32_t)rl << 16) | (uint32_t)rk;
-                if (node >= 0) {
-                    ws.gnodeseg[node] = (R0 + rl) * g.nTx + tx;
-                    ws.gnoderank[node] = rk;
-                }
-            } else {
-                comprank[c] = 0xFFFFFFFFu;
+        uint32_t wt;
+        const int pre = (int)warp_excl_scan((uint32_t)sum, wt);
+        if (lane == 0) sm.wsum[w] = (int)wt;
+        __syncthreads();
+        int off = 0, all = 0;
+#pragma unroll
+        for (int i = 0; i < KN_WARPS; i++) {
+            off += i < w ? sm.wsum[i] : 0;
+            all += sm.wsum[i];
+        }
+        int run = carry + off + pre;
+#pragma unroll
+        for (int i = 0; i < KN_ITEMS; i++) {
+            if (i0 + i < nS) ws.segoff[sbase + i0 + i] = run;
+            run += v[i];
+        }
+        carry += all;
+        __syncthreads();  // wsum reuse
+    }
+    // descriptor: bits 62-63 status (1 aggregate, 2 inclusive prefix), low 32
+    // bits value.  Warp 0 looks back over 32 predecessors at a time.
+    if (w == 0) {
+        if (lane == 0)
+            atomicExch(ws.scanstate + ty, ((ty == 0 ? 2ull : 1ull) << 62) | (uint32_t)carry);
+        int excl = 0;
+        if (ty > 0) {
+            const volatile unsigned long long *st = ws.scanstate;
+            int j = ty - 1;
+            while (true) {
+                const int idx = j - lane;
+                const unsigned long long d = idx >= 0 ? st[idx] : (2ull << 62);
+                const unsigned s2 = (unsigned)(d >> 62);
+                const uint32_t incl = __ballot_sync(FULL, s2 == 2), zero = __ballot_sync(FULL, s2 == 0);
+                const int first = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive prefix
+                const uint32_t need = (2u << first) - 1u;         // lanes 0..first
+                if (zero & need) continue;                        // not all published yet: spin
+                int v = lane <= first ? (int)(uint32_t)d : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                excl += v;
+                if (incl) break;
+                j -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicExch(ws.scanstate + ty, (2ull << 62) | (uint32_t)(excl + carry));
             }
         }
-        run += __popc(bal);
+        if (lane == 0) {
+            sm.excl = excl;
+            if (ty == g.nTy - 1) *n_components = excl + carry;
+        }
+    }
+    __syncthreads();
+    const int excl = sm.excl;
+    // ---- phase 3: labels of the roots (components and border nodes)
+    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
+        const int tile = ty * g.nTx + tx;
+        const int32_t *meta = ws.meta + (int64_t)tile * META;
+        const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
+        const int nbw = (ncomp + 31) >> 5;
+        uint32_t *bits = sm.nrbits[w];
+        int32_t *wpre = sm.wpre[w], *rf = sm.rowfirst[w], *rb = sm.rbase[w];
+        const int nodebase = tile * g.capb;
+        kn_nonroots(ws, nodebase, nborder, bits, nbw, sm.nrrow[w], true);
+        for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
+            const int j = j0 + lane;
+            const uint32_t pc = j < nbw ? __popc(bits[j]) : 0u;
+            uint32_t tot;
+            const int pre = (int)warp_excl_scan(pc, tot);
+            if (j < nbw) wpre[j] = acc + pre;
+            acc += (int)tot;
+        }
+        {
+            uint32_t tot;
+            const int nrp = (int)warp_excl_scan((uint32_t)sm.nrrow[w][lane], tot);
+            const int f = __ldcg(meta + META_ROWFIRST + lane);
+            rf[lane] = f;
+            if (lane == 0) rf[TH] = ncomp;
+            const int so = lane < rows ? __ldcg(ws.segoff + sbase + (int64_t)lane * g.nTx + tx) : 0;
+            // label(c) = excl + segoff + (roots before c in the tile) - (roots
+            // in earlier rows) + 1, roots before c = c - nonroots before c
+            rb[lane] = excl + so - (f - nrp) + 1;
+        }
+        __syncwarp();
+        auto nonroots_before = [&](int c) -> int {
+            return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
+        };
+        auto row_of = [&](int c) -> int {
+            int r = 0;
+#pragma unroll
+            for (int step = TH / 2; step > 0; step >>= 1)
+                if (r + step < rows && rf[r + step] <= c) r += step;
+            return r;
+        };
+        int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+        for (int c = lane; c < ncomp; c += 32) {
+            if ((bits[c >> 5] >> (c & 31)) & 1u) continue;  // K4 writes it
+            complab[c] = rb[row_of(c)] + c - nonroots_before(c);
+        }
+        for (int j = lane; j < nborder; j += 32) {
+            const int node = nodebase + j;
+            if (__ldcg(ws.gparent + node) != node) continue;
+            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
+            ws.gnodelab[node] = rb[gc >> 16] + c - nonroots_before(c);
+        }
+        __syncwarp();
     }
 }
 
 // ========================================================================= K4
-// Single-pass decoupled-lookback exclusive scan of segcnt -> segoff, in the
-// raster order of the segments; partitions are claimed through a ticket so
-// a partition only ever waits on partitions that are already running.
-// Descriptor: bits 62-63 status (1 aggregate, 2 inclusive prefix), low 32 bits value.
-__global__ void __launch_bounds__(SCAN_THREADS)
-k_scan(Geometry g, Workspace ws, int32_t *n_components) {
-    __shared__ int s_part, s_excl;
-    __shared__ int wsum[SCAN_THREADS / 32];
-    if (threadIdx.x == 0) s_part = atomicAdd(ws.ticket, 1);
-    __syncthreads();
-    const int part = s_part;
-    const int64_t base = (int64_t)part * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
-    int v[SCAN_ITEMS];
-    int sum = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-        int64_t k = base + i;
-        v[i] = k < g.nseg ? ws.segcnt[k] : 0;
-        sum += v[i];
-    }
-    uint32_t wt;
-    int pre = (int)warp_excl_scan((uint32_t)sum, wt);
-    const int wid = threadIdx.x >> 5;
-    if (lane_id() == 0) wsum[wid] = (int)wt;
-    __syncthreads();
-    int off = 0, agg = 0;
-    for (int i = 0; i < SCAN_THREADS / 32; i++) {
-        off += i < wid ? wsum[i] : 0;
-        agg += wsum[i];
-    }
-    if (threadIdx.x == 0) {
-        volatile unsigned long long *st = ws.scanstate;
-        if (part == 0) {
-            atomicExch(ws.scanstate, (2ull << 62) | (uint32_t)agg);
-            s_excl = 0;
-        } else {
-            atomicExch(ws.scanstate + part, (1ull << 62) | (uint32_t)agg);
-            int excl = 0;
-            int j = part - 1;
-            while (true) {
-                unsigned long long d = st[j];
-                unsigned s = (unsigned)(d >> 62);
-                if (s == 0) continue;  // predecessor not published yet: spin
-                excl += (int)(uint32_t)d;
-                if (s == 2) break;
-                j--;
-            }
-            __threadfence();
-            atomicExch(ws.scanstate + part, (2ull << 62) | (uint32_t)(excl + agg));
-            s_excl = excl;
-        }
-        if (part == g.nscan - 1) *n_components = s_excl + agg;
-    }
-    __syncthreads();
-    int run = s_excl + off + pre;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; i++) {
-        int64_t k = base + i;
-        if (k < g.nseg) ws.segoff[k] = run;
-        run += v[i];
-    }
-}
-
-// ======================================================================== K4b
-// One warp per tile: the final label of every tile component, i.e.
-// flatten's consecutive numbering in raster order: a root
-// gets its segment's offset + its rank + 1; a border component that is not a
-// root gets its global root's label.
+// A border component that is not a global root takes its root's label (a
+// root of this image's forest, or -- row bands -- a root owned by another
+// band, whose global label arrived in xlab; labels stored here are band-local,
+// K5 adds the band offset).  One warp per tile, over its border nodes.
 __global__ void __launch_bounds__(256)
-k_final(Geometry g, Workspace ws) {
+k_fixup(Geometry g, Workspace ws, int32_t boff) {
     const int lane = lane_id();
     const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (tile >= g.nT) return;
-    const int tx = tile % g.nTx, R0 = (tile / g.nTx) * TH;
-    const int ncomp = ws.meta[(int64_t)tile * META + META_NCOMP];
-    const uint32_t *comprank = ws.comprank + (int64_t)tile * CAPC;
-    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
-    int32_t *complab = ws.complab + (int64_t)tile * CAPC;
-    const int32_t off = ws.boff ? *ws.boff : 0;
-    for (int c0 = 0; c0 < ncomp; c0 += 64) {
-        // two components per lane in flight
-        const int ca = c0 + lane, cb = c0 + 32 + lane;
-        const uint32_t ra = ca < ncomp ? comprank[ca] : 0u, rb = cb < ncomp ? comprank[cb] : 0u;
-        int la = 0, lb = 0;
-        if (ca < ncomp) {
-            if (ra != 0xFFFFFFFFu) {
-                la = off + ws.segoff[(int64_t)(R0 + (int)(ra >> 16)) * g.nTx + tx] + (int)(ra & 0xFFFF) + 1;
-            } else {
-                la = node_label(ws, gfind_ro(ws.gparent, compnode[ca]), off);
-            }
-        }
-        if (cb < ncomp) {
-            if (rb != 0xFFFFFFFFu) {
-                lb = off + ws.segoff[(int64_t)(R0 + (int)(rb >> 16)) * g.nTx + tx] + (int)(rb & 0xFFFF) + 1;
-            } else {
-                lb = node_label(ws, gfind_ro(ws.gparent, compnode[cb]), off);
-            }
-        }
-        if (ca < ncomp) complab[ca] = la;
-        if (cb < ncomp) complab[cb] = lb;
+    const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
+    const int nodebase = tile * g.capb;
+    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+    for (int j = lane; j < nborder; j += 32) {
+        const int node = nodebase + j;
+        if (__ldcg(ws.gparent + node) == node) continue;
+        const int r = gfind_ro(ws.gparent, node);
+        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : ws.xlab[-2 - r] - boff;
+        complab[__ldcg(ws.gnodecomp + node) & 0xFFFF] = lab;
     }
 }
 
@@ -845,8 +887,8 @@ k_final(Geometry g, Workspace ws) {
 // j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
 // warp is one contiguous 512-byte stretch of the output row.
 constexpr int K5_WARPS = 8;
-__global__ void __launch_bounds__(K5_WARPS * 32)
-k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
+__global__ void __launch_bounds__(K5_WARPS * 32, 8)
+k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
     __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
     const int lane = lane_id(), wi = threadIdx.x >> 5;
     const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
@@ -863,9 +905,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     int32_t *rowlab = s_lab[wi];
     {
-        const uint16_t *rc = ws.runcomp + seg * MAXRUN;
-        const int32_t *complab = ws.complab + (int64_t)tile * CAPC;
-        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)];
+        const uint16_t *rc = ws.runcomp + seg * g.maxrun;
+        const int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+#pragma unroll 1
+        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)] + off;
     }
     __syncwarp();
     int32_t *out = labels + (int64_t)row * g.W + C0;
@@ -914,8 +957,8 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
-    const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * MAXRUN;
-    const int32_t *compnode = ws.compnode + (int64_t)tile * CAPC;
+    const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * g.maxrun;
+    const int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     for (int b = 0; b < 32; b++) {
         const int c = C0 + 32 * lane + b;
         if (c >= g.W) break;
@@ -936,11 +979,11 @@ __global__ void k_band_apply(int32_t *gparent, const int2 *act, int n) {
     if (i < n) gparent[act[i].x] = act[i].y;
 }
 
-__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out) {
+__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int32_t boff) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= g.W) return;
     const int n = nodes[c];
-    out[c] = (n >= 0 && __ldcg(ws.gparent + n) == n) ? node_label(ws, n, *ws.boff) : -1;
+    out[c] = (n >= 0 && __ldcg(ws.gparent + n) == n) ? __ldcg(ws.gnodelab + n) + boff : -1;
 }
 
 // ==================================================================== host
@@ -950,7 +993,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 7 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+    return 4 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
 static cudaError_t set_attrs() {
@@ -968,15 +1011,8 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };
-    mark(K_PACK);
-    {
-        const int64_t words = (int64_t)g.H * g.WW;
-        k_pack<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(img, g, ws.bm);
-        mark(K_FILL);
-        k_fill<<<(unsigned)((words + 255) / 256), 256, 0, stream>>>(g, ws.bm, ws.fm);
-    }
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(g, ws, g_k1_stop, g_k1_exper);
+    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(img, g, ws, g_k1_stop, g_k1_exper);
     mark(K_BORDER);
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
@@ -987,25 +1023,20 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
 
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev) {
-    auto mark = [&](int i) {
-        if (ev) cudaEventRecord(ev[i], stream);
-    };
-    mark(K_ROOTS);
-    k_roots<<<(g.nT + K3_WARPS - 1) / K3_WARPS, K3_WARPS * 32, 0, stream>>>(g, ws);
-    mark(K_SCAN);
-    k_scan<<<g.nscan, SCAN_THREADS, 0, stream>>>(g, ws, n_components);
+    if (ev) cudaEventRecord(ev[K_NUMBER], stream);
+    k_number<<<g.nTy, KN_WARPS * 32, 0, stream>>>(g, ws, n_components);
     return cudaGetLastError();
 }
 
-cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels, int32_t boff,
                             cudaStream_t stream, cudaEvent_t *ev) {
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };
-    mark(K_FINAL);
-    k_final<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws);
+    mark(K_FIXUP);
+    k_fixup<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws, boff);
     mark(K_WRITE);
-    k_write<<<(unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream>>>(g, ws, labels);
+    k_write<<<(unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream>>>(g, ws, labels, boff);
     mark(K_COUNT);
     return cudaGetLastError();
 }
@@ -1015,7 +1046,7 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
                          cudaEvent_t *ev) {
     cudaError_t e = run_stage_local(g, ws, img, stream, ev);
     if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev);
-    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev);
+    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, 0, stream, ev);
     return e;
 }
 
@@ -1031,8 +1062,8 @@ cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t
 }
 
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
-                        int32_t *labels_out, cudaStream_t stream) {
-    k_band_export<<<(g.W + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out);
+                        int32_t *labels_out, int32_t boff, cudaStream_t stream) {
+    k_band_export<<<(g.W + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out, boff);
     return cudaGetLastError();
 }
 

@@ -12,5 +12,5 @@ for stop, ex in [(1, 0), (2, 0), (99, 0)]:
     plan.set_profiling(20)
     for _ in range(23): plan.label(img, out, n)
     t = plan.kernel_times()
-    print(f"{name} stop={stop:2d} k_pack {t['k_pack']*1000:7.1f} us  k_tile_local {t['k_tile_local']*1000:8.1f} us  total {sum(t.values())*1000:8.1f} us")
+    print(f"{name} stop={stop:2d} k_tile_local {t['k_tile_local']*1000:8.1f} us  total {sum(t.values())*1000:8.1f} us")
 ccl._L.ccl_debug_set(1, 99); ccl._L.ccl_debug_set(2, 0)

@@ -75,6 +75,17 @@ def test_nonbinary_bytes():
     assert_same(img, "bytes")
 
 
+@pytest.mark.gpu
+def test_nonbinary_bytes_aligned():
+    # W % 16 == 0 takes the 16-byte vector path of K1's foreground predicate;
+    # every byte value 0..255 appears at every position of a 16-byte vector
+    rng = np.random.default_rng(10)
+    vals = np.arange(256, dtype=np.uint8)
+    img = rng.permutation(np.tile(vals, 300 * 2048 // 256)).reshape(300, 2048)
+    img = (img * (rng.random((300, 2048)) < 0.45)).astype(np.uint8)
+    assert_same(img, "bytes16")
+
+
 def _mosaic(h, w, gap, off_r, off_c, cols):
     """Every h x w binary pattern once, separated by `gap` background pixels and
     shifted by (off_r, off_c) so patterns straddle tile edges."""
@@ -133,7 +144,7 @@ def test_kernel_times_profiling():
     plan.set_profiling(1)
     plan.label(img)
     t = plan.kernel_times()
-    assert set(t) == {"k_pack", "k_fill", "k_tile_local", "k_border", "k_roots", "k_scan", "k_final", "k_write"}
+    assert set(t) == {"k_tile_local", "k_border", "k_number", "k_fixup", "k_write"}
     assert all(v >= 0 for v in t.values())
 
 
