@@ -259,41 +259,26 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
 }
 
 // ========================================================================= K1
-// Tile-local two-pass labeling with runs as the provisional labels.  A run's
-// index k (row-major over the tile) plays the role of ARemSP's provisional
-// label: indices grow in raster order of the runs' heads, so "link to the
-// smaller index" keeps every root at its component's first pixel.
+// Tile-local two-pass labeling with runs as the provisional labels.  The run
+// with ordinal o in tile row r has index k = r*MAXRUN + o; indices grow in
+// raster order of the runs' heads and play the role of ARemSP's provisional
+// labels, so "link to the smaller index" keeps every root at its component's
+// first pixel.  Every warp owns S consecutive rows (a strip); per-run work is
+// done a row at a time with lane = run ordinal.
 struct K1Smem {
     uint16_t p[RCAP];              // parent of each run (the union-find array p of Alg. merge)
-    uint32_t bm[TH][WPR];          // row masks
-    uint32_t hd[TH][WPR];          // run heads per lane word
-    uint32_t mc[TH][WPR];          // upper-side merge heads per lane word
+    uint32_t bm[TH][WPR];          // run masks (foreground + filled holes)
+    // P0: raw foreground; P2a/P2b: upper-side merge heads; P3 on: bitmap of
+    // the roots of components that touch the tile border (run k = r*MAXRUN+o
+    // -> word [r][o/32], so every warp clears exactly the words it read)
+    uint32_t mc[TH][WPR];
     uint16_t hbase[TH][WPR];       // runs whose head lies in earlier words of the row
     int32_t nrun[TH];              // runs per row
-    int32_t rowbase[TH + 1];       // runs in earlier rows
     int32_t rowcnt[TH];            // components whose root run lies in the row
-    int32_t wscan[NW];             // block-scan scratch
+    int32_t bcnt[TH];              // border components whose root run lies in the row
 };
 
-// Block-wide exclusive scan of one int per thread (NW warps); returns prefix,
-// sets total.
-__device__ __forceinline__ int block_excl_scan(int v, int *scratch, int &total) {
-    uint32_t tot;
-    int pre = (int)warp_excl_scan((uint32_t)v, tot);
-    const int w = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane_id() == 0) scratch[w] = (int)tot;
-    __syncthreads();
-    int off = 0, all = 0;
-#pragma unroll
-    for (int i = 0; i < NW; i++) {
-        int s = scratch[i];
-        off += i < w ? s : 0;
-        all += s;
-    }
-    total = all;
-    return pre + off;
-}
+__device__ __forceinline__ int kidx(int r, int o) { return r * MAXRUN + o; }
 
 // Upper-side edges that the copy step does not already cover.  The edge set
 // {(L, leftmost upper run of L)} U {(U, leftmost lower run of U)} connects
@@ -324,8 +309,8 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
     return ((u << 2) | (up >> 30)) & ((d << 1) | (dp >> 31));
 }
 
-__global__ void __launch_bounds__(NW * 32, 4)
-k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop, int exper) {
+__global__ void __launch_bounds__(NW * 32, 5)
+k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
 
@@ -338,12 +323,28 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
     const int gword = tx * WPR + lane;  // this lane's word index in the image row
     const int r0 = w * S;
     volatile uint16_t *vp = sm.p;
+    uint32_t *bbits = &sm.mc[0][0];
 
     if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
         for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
     }
-    if (threadIdx.x < TH) sm.rowcnt[threadIdx.x] = 0;
+    // Warm L2 with the pixels of the tile that will start about one wave of
+    // resident CTAs later (pfd = resident CTAs on the device): its loads then
+    // hit L2 instead of waiting on HBM.
+    {
+        const int pt = blockIdx.x + pfd;
+        if (pfd > 0 && pt < g.nT) {
+            const int prow = (pt / g.nTx) * TH + (threadIdx.x >> 3);
+            const int pcol = (pt % g.nTx) * TW + (threadIdx.x & 7) * 128;
+            if (prow < g.H && pcol < g.W) {
+                const uint8_t *a = img + (int64_t)prow * g.W + pcol;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                if ((threadIdx.x & 7) == 7 && pcol + 127 < g.W)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + 127));
+            }
+        }
+    }
     // ---- P0: the pixels of the tile, read once with 16-byte streaming loads:
     // fg = byte != 0 (reading A10), one bit per pixel.  The
     // warp's S rows are all in flight before the first is used.
@@ -356,13 +357,16 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         sm.mc[r0 + i][lane] = xs[i];  // raw masks (mc is free until P2a)
         if (r0 + i < rows && gword < g.WW) ws.bm[(int64_t)(R0 + r0 + i) * g.WW + gword] = xs[i];
     }
+    if (lane < S) sm.bcnt[r0 + lane] = 0;
     __syncthreads();
+    if (stop < 0) return;
     // ---- P0b: run mask = foreground + bridged single-pixel holes (a background
     // pixel whose left and right neighbours and the pixel above or below are
     // foreground).  Only holes whose neighbours lie in
     // this tile are filled: any subset of bridged holes preserves the
     // partition of the foreground, and K2/K5 read the same run mask.
-    // Then run heads and per-word run counts.
+    // Then run heads, per-word run counts, and every run starts as its own
+    // label.
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
@@ -379,41 +383,25 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         uint32_t nr;
         const uint32_t base = warp_excl_scan(__popc(hx), nr);
         sm.bm[rl][lane] = x;
-        sm.hd[rl][lane] = hx;
         sm.hbase[rl][lane] = (uint16_t)base;
         if (lane == 0) sm.nrun[rl] = (int)nr;
+#pragma unroll 1
+        for (int o = lane; o < (int)nr; o += 32) vp[kidx(rl, o)] = (uint16_t)kidx(rl, o);
     }
     __syncthreads();
-    if (w == 0) {
-        uint32_t tot;
-        const int pre = (int)warp_excl_scan((uint32_t)sm.nrun[lane], tot);
-        sm.rowbase[lane] = pre;
-        if (lane == 31) sm.rowbase[TH] = (int)tot;
-    }
-    __syncthreads();
-    const int R = sm.rowbase[TH];
     if (stop <= 0) return;
 
-    // ---- P2a: scan.  Every run starts as a new label; a
-    // run with a foreground pixel among the three above any of its pixels
-    // instead copies its leftmost upper neighbour's label (the decision
+    // ---- P2a: scan.  A run with a foreground pixel among the three above any
+    // of its pixels copies its leftmost upper neighbour's label (the decision
     // tree's copy(b)/copy(a)/copy(c)).  Each warp walks its
     // own rows in order, so inside a strip a run copies its upper neighbour's
     // parent (already final within the strip); a strip's first row copies the
-    // raw run index of the strip above.
+    // upper run's index (a run of the strip above).
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
-        if (rl >= rows) {
+        if (rl >= rows || rl == 0) {
             sm.mc[rl][lane] = 0u;
-            continue;
-        }
-        const int rb = sm.rowbase[rl], re = sm.rowbase[rl + 1];
-#pragma unroll 1
-        for (int k = rb + lane; k < re; k += 32) vp[k] = (uint16_t)k;
-        if (rl == 0) {
-            sm.mc[rl][lane] = 0u;
-            __syncwarp();
             continue;
         }
         const uint32_t x = sm.bm[rl][lane], u = sm.bm[rl - 1][lane];
@@ -421,10 +409,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         const uint32_t upr = __shfl_up_sync(FULL, u, 1), unr = __shfl_down_sync(FULL, u, 1);
         const uint32_t xp = lane == 0 ? 0u : xpr;
         const uint32_t up = lane == 0 ? 0u : upr, un = lane == 31 ? 0u : unr;
-        const uint32_t hx = sm.hd[rl][lane];
+        const uint32_t hx = x & ~((x << 1) | (xp >> 31));
         // upper row: heads and run-index base of lanes lane-1, lane, lane+1
-        const uint32_t hu = sm.hd[rl - 1][lane];
-        const int ub = sm.rowbase[rl - 1] + sm.hbase[rl - 1][lane];
+        const uint32_t hu = u & ~((u << 1) | (up >> 31));
+        const int ub = kidx(rl - 1, sm.hbase[rl - 1][lane]);
         const uint32_t hup = __shfl_up_sync(FULL, hu, 1), hun = __shfl_down_sync(FULL, hu, 1);
         const int ubp = __shfl_up_sync(FULL, ub, 1), ubn = __shfl_down_sync(FULL, ub, 1);
         const uint32_t uL = (u << 1) | (up >> 31);  // upper pixel at p-1
@@ -437,9 +425,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         uint32_t mc = upper_merge_heads(hu, u, up, x, xp, S_);
         if (rl >= 2) mc &= ~hole_bridged(u, up, sm.bm[rl - 2][lane]);
         sm.mc[rl][lane] = mc;
-        const int lbase = rb + sm.hbase[rl][lane] - 1;
+        const int lbase = kidx(rl, sm.hbase[rl][lane]) - 1;
         const bool instrip = i > 0;
-        __syncwarp();
         while (ft) {
             const int b = __ffs(ft) - 1;
             ft &= ft - 1;
@@ -457,29 +444,23 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
         __syncwarp();
     }
     __syncthreads();
-    // ---- P3a: resolve the copies across strips, strip by strip (Alg. flatten's
-    // increasing order): a run of strip s points at a root of
-    // strip s or at a run of strip s-1, which is final once strip s-1 is done.
-    for (int st = 1; st < NW; st++) {
-        const int kb = sm.rowbase[min(st * S, TH)], ke = sm.rowbase[min(st * S + S, TH)];
-        for (int k = kb + (int)threadIdx.x; k < ke; k += NW * 32) {
-            const uint32_t pk = vp[k];
-            if ((int)pk < kb) vp[k] = vp[pk];
-        }
-        __syncthreads();
-    }
     if (stop <= 1) return;
     // ---- P2b: the remaining edges, merged with lock-free Rem's splicing
-    // (the decision tree's copy(c,a)/copy(c,d) merges)
+    // (the decision tree's copy(c,a)/copy(c,d) merges).  The
+    // parent chains may still cross strips (a strip's first row points into
+    // the strip above): Rem's algorithm works on any forest with p[x] <= x.
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
-        if (m == 0u) continue;
-        const uint32_t hu = sm.hd[rl - 1][lane];
-        const int ub = sm.rowbase[rl - 1] + sm.hbase[rl - 1][lane];
-        const int xb = sm.rowbase[rl] + sm.hbase[rl][lane];
-        const uint32_t hx = sm.hd[rl][lane];
+        sm.mc[rl][lane] = 0u;  // becomes this row's part of bbits
+        if (__ballot_sync(FULL, m != 0u) == 0u) continue;  // warp-uniform
+        const uint32_t u = sm.bm[rl - 1][lane], x = sm.bm[rl][lane];
+        const uint32_t upr = __shfl_up_sync(FULL, u, 1), xpr = __shfl_up_sync(FULL, x, 1);
+        const uint32_t hu = u & ~((u << 1) | (lane == 0 ? 0u : (upr >> 31)));
+        const int ub = kidx(rl - 1, sm.hbase[rl - 1][lane]);
+        const int xb = kidx(rl, sm.hbase[rl][lane]);
+        const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xpr >> 31)));
         while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
@@ -492,118 +473,115 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop
     __syncthreads();
     if (stop <= 2) return;
     // ---- P3: flatten -- every run -> its root (Alg. flatten's p[i] <- p[p[i]],
-    // PAPER.md:711-712); roots in index order = raster order of first pixels
-    // get the consecutive component numbers (Alg. flatten's k++)
-    const int per = (R + NW * 32 - 1) / (NW * 32);
-    const int k0 = threadIdx.x * per, k1 = min(R, k0 + per);
-    int cnt = 0;
-    for (int k = k0; k < k1; k++) {
-        uint32_t r = vp[k];
-        while (vp[r] != r) r = vp[r];
-        vp[k] = (uint16_t)r;
-        cnt += r == (uint32_t)k;
-    }
-    int ncomp;
-    int cidx = block_excl_scan(cnt, sm.wscan, ncomp);
-    // row of run k0: the last row whose base is <= k0
-    int rl0 = 0;
-#pragma unroll
-    for (int step = TH / 2; step > 0; step >>= 1)
-        if (sm.rowbase[rl0 + step] <= k0) rl0 += step;
-    {
-        int rl = rl0, run = 0;
-        for (int k = k0; k < k1; k++) {
-            if (sm.p[k] != (uint16_t)k) continue;
-            while (sm.rowbase[rl + 1] <= k) {
-                if (run) atomicAdd(&sm.rowcnt[rl], run);
-                run = 0;
-                rl++;
+    // PAPER.md:711-712), own rows, lane = run ordinal.  Roots per row; a run on
+    // the tile border marks its root in bbits, and the first mark of a root
+    // counts it in its row's border-root count (row of run r = r / MAXRUN).
+    const int lc = vcols - 1;
+#pragma unroll 1
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i, n = sm.nrun[rl];
+        const bool edge_row = rl == 0 || rl == rows - 1;
+        const bool lfirst = sm.bm[rl][0] & 1u, llast = (sm.bm[rl][lc >> 5] >> (lc & 31)) & 1u;
+        int cnt = 0;
+#pragma unroll 1
+        for (int o0 = 0; o0 < n; o0 += 32) {
+            const int o = o0 + lane, k = kidx(rl, o);
+            bool root = false;
+            if (o < n) {
+                // the first hop is usually shared: later rows of the strip
+                // copied the same upper-strip run, so it is compressed too
+                const uint32_t j = vp[k];
+                uint32_t r = j;
+                while (vp[r] != r) r = vp[r];
+                vp[k] = (uint16_t)r;
+                if (j != r) vp[j] = (uint16_t)r;
+                root = r == (uint32_t)k;
+                if (edge_row || (o == 0 && lfirst) || (o == n - 1 && llast)) {
+                    const uint32_t bit = 1u << (r & 31);
+                    uint32_t *wd = bbits + (r / MAXRUN) * WPR + ((r % MAXRUN) >> 5);
+                    if (!(atomicOr(wd, bit) & bit)) atomicAdd(&sm.bcnt[r / MAXRUN], 1);
+                }
             }
-            run++;
-            sm.p[k] = (uint16_t)(0x8000 | cidx++);  // root: flag | component
+            cnt += __popc(__ballot_sync(FULL, root));
         }
-        if (run) atomicAdd(&sm.rowcnt[rl], run);
+        if (lane == 0) sm.rowcnt[rl] = cnt;
     }
     __syncthreads();
     if (stop <= 3) return;
-    int32_t *meta = ws.meta + (int64_t)tile * META;
-    if (w == 0) {  // first component of every tile row (components are in key order)
-        uint32_t tot;
-        const int pre = (int)warp_excl_scan((uint32_t)sm.rowcnt[lane], tot);
-        meta[META_ROWFIRST + lane] = pre;
-        if (lane == 0) meta[META_ROWFIRST + TH] = (int)tot;
+    // ---- P3b: roots in index order = raster order of first pixels get the
+    // consecutive component numbers (Alg. flatten's k++):
+    // component = (roots in earlier rows) + (roots before it in its row).
+    // Border roots become nodes of the global union-find in the same order;
+    // key = (image row, tile column, run ordinal): raster order.
+    uint32_t rtot, btot;
+    const int rowfirst = (int)warp_excl_scan((uint32_t)sm.rowcnt[lane], rtot);  // lane = row
+    const int bfirst = (int)warp_excl_scan((uint32_t)sm.bcnt[lane], btot);
+    const int ncomp = (int)rtot, nborder = (int)btot;
+    int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
+    const int nodebase = tile * g.capb;
+#pragma unroll 1
+    for (int i = 0; i < S; i++) {
+        const int rl = r0 + i, n = sm.nrun[rl];
+        int c = __shfl_sync(FULL, rowfirst, rl), bi = __shfl_sync(FULL, bfirst, rl);
+        const uint32_t *brow = bbits + rl * WPR;
+#pragma unroll 1
+        for (int o0 = 0; o0 < n; o0 += 32) {
+            const int o = o0 + lane, k = kidx(rl, o);
+            const bool root = o < n && vp[k] == (uint32_t)k;
+            const bool broot = root && ((brow[o >> 5] >> (o & 31)) & 1u);
+            const uint32_t bal = __ballot_sync(FULL, root), bbal = __ballot_sync(FULL, broot);
+            const uint32_t lt = (1u << lane) - 1u;
+            if (root) {
+                const int ci = c + __popc(bal & lt);
+                vp[k] = (uint16_t)(0x8000u | (uint32_t)ci);
+                if (broot) {
+                    const int node = nodebase + bi + __popc(bbal & lt);
+                    compnode[ci] = node;
+                    ws.gparent[node] = node;
+                    ws.gnodecomp[node] = (rl << 16) | ci;
+                    ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
+                }
+            }
+            c += __popc(bal);
+            bi += __popc(bbal);
+        }
     }
+    __syncthreads();
+    if (stop <= 4) return;
     auto comp_of = [&](int k) -> int {
         const uint32_t pk = sm.p[k];
         return (int)((pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu));
     };
-    auto root_of = [&](int k) -> int {
-        const uint32_t pk = sm.p[k];
-        return (pk & 0x8000u) ? k : (int)pk;
-    };
-    // ---- P4a: component of every run (for K5); mark the components that
-    // touch the tile border (flag 0x4000 on the root)
-#pragma unroll
+    // ---- P4a: component of every run (for K5)
+#pragma unroll 1
     for (int i = 0; i < S; i++) {
-        const int rl = r0 + i;
-        if (rl >= rows) break;
-        const int b = sm.rowbase[rl], n = sm.nrun[rl];
+        const int rl = r0 + i, n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
 #pragma unroll 1
-        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(b + o);
+        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(kidx(rl, o));
     }
-    auto mark = [&](int k) {
-        const int r = root_of(k);
-        atomicOr(reinterpret_cast<unsigned int *>(sm.p) + (r >> 1), 0x4000u << (16 * (r & 1)));
-    };
-    const int lc = vcols - 1;
-    for (int k = threadIdx.x; k < sm.rowbase[1]; k += NW * 32) mark(k);
-    for (int k = sm.rowbase[rows - 1] + threadIdx.x; k < sm.rowbase[rows]; k += NW * 32) mark(k);
-    for (int r = threadIdx.x; r < rows; r += NW * 32) {
-        if (sm.bm[r][0] & 1u) mark(sm.rowbase[r]);
-        if ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) mark(sm.rowbase[r + 1] - 1);
-    }
-    __syncthreads();
-    if (stop <= 4) return;
-    // ---- P4b: border components -> global union-find nodes
-    int bc = 0;
-    for (int k = k0; k < k1; k++) bc += (sm.p[k] & 0xC000u) == 0xC000u;
-    int nborder;
-    int bidx = block_excl_scan(bc, sm.wscan, nborder);
-    int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
-    const int nodebase = tile * g.capb;
-    {
-        int rl = rl0;
-        for (int k = k0; k < k1; k++) {
-            const uint32_t pk = sm.p[k];
-            if ((pk & 0xC000u) != 0xC000u) continue;
-            while (sm.rowbase[rl + 1] <= k) rl++;
-            const int c = (int)(pk & 0x3FFFu);
-            const int node = nodebase + bidx++;
-            compnode[c] = node;
-            ws.gparent[node] = node;
-            ws.gnodecomp[node] = (rl << 16) | c;
-            // global order = (image row, tile column, run ordinal): raster order
-            ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + (k - sm.rowbase[rl]);
-        }
-    }
-    __syncthreads();
-    if (stop <= 5) return;
     // ---- P4c: nodes of the border pixels (for K2)
     {
-        const int ntop = sm.nrun[0], bb = sm.rowbase[rows - 1], nbot = sm.nrun[rows - 1];
-        for (int o = threadIdx.x; o < ntop; o += NW * 32) ws.topnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(o)];
-        for (int o = threadIdx.x; o < nbot; o += NW * 32) ws.botnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(bb + o)];
+        const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
+        for (int o = threadIdx.x; o < ntop; o += NW * 32)
+            ws.topnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(kidx(0, o))];
+        for (int o = threadIdx.x; o < nbot; o += NW * 32)
+            ws.botnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(kidx(rows - 1, o))];
         for (int r = threadIdx.x; r < rows; r += NW * 32) {
             const int64_t off = (int64_t)tx * g.H + R0 + r;
-            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? compnode[comp_of(sm.rowbase[r])] : -1;
-            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? compnode[comp_of(sm.rowbase[r + 1] - 1)] : -1;
+            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? compnode[comp_of(kidx(r, 0))] : -1;
+            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? compnode[comp_of(kidx(r, sm.nrun[r] - 1))] : -1;
         }
     }
-    if (threadIdx.x == 0) {
-        meta[META_NCOMP] = ncomp;
-        meta[META_NBORDER] = nborder;
-        meta[META_ROWS] = rows;
+    int32_t *meta = ws.meta + (int64_t)tile * META;
+    if (w == 0) {  // first component of every tile row (components are in key order)
+        meta[META_ROWFIRST + lane] = rowfirst;
+        if (lane == 0) {
+            meta[META_ROWFIRST + TH] = ncomp;
+            meta[META_NCOMP] = ncomp;
+            meta[META_NBORDER] = nborder;
+            meta[META_ROWS] = rows;
+        }
     }
 }
 
@@ -718,7 +696,7 @@ __device__ __forceinline__ void kn_nonroots(const Workspace &ws, int nodebase, i
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(KN_WARPS * 32, 4)
+__global__ void __launch_bounds__(KN_WARPS * 32, 6)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
     __shared__ KNSmem sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
@@ -838,17 +816,12 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         auto nonroots_before = [&](int c) -> int {
             return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
         };
-        auto row_of = [&](int c) -> int {
-            int r = 0;
-#pragma unroll
-            for (int step = TH / 2; step > 0; step >>= 1)
-                if (r + step < rows && rf[r + step] <= c) r += step;
-            return r;
-        };
         int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+        int r = 0;  // row of component c: components are in row order, so it only grows
         for (int c = lane; c < ncomp; c += 32) {
+            while (r + 1 < rows && rf[r + 1] <= c) r++;
             if ((bits[c >> 5] >> (c & 31)) & 1u) continue;  // K4 writes it
-            complab[c] = rb[row_of(c)] + c - nonroots_before(c);
+            complab[c] = rb[r] + c - nonroots_before(c);
         }
         for (int j = lane; j < nborder; j += 32) {
             const int node = nodebase + j;
@@ -996,12 +969,21 @@ int pipeline_launches(const Geometry &g) {
     return 4 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
+static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k_tile_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(K1Smem));
-    if (e == cudaSuccess) g_attr_done = true;
-    return e;
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local, NW * 32,
+                                                           sizeof(K1Smem))) != cudaSuccess)
+        return e;
+    g_k1_resident = sms * per;
+    g_attr_done = true;
+    return cudaSuccess;
 }
 
 cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
@@ -1012,8 +994,9 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(img, g, ws, g_k1_stop, g_k1_exper);
+    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(img, g, ws, g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
     mark(K_BORDER);
+    if (g_k1_stop < 99) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
     const int64_t warps = nh + (nv + 31) / 32;
@@ -1045,6 +1028,10 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev) {
     cudaError_t e = run_stage_local(g, ws, img, stream, ev);
+    if (g_k1_stop < 99) {  // development knob: K1 truncated, the rest would read garbage
+        for (int i = K_NUMBER; ev && i <= K_COUNT; i++) cudaEventRecord(ev[i], stream);
+        return e;
+    }
     if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev);
     if (e == cudaSuccess) e = run_stage_final(g, ws, labels, 0, stream, ev);
     return e;
