@@ -276,6 +276,7 @@ struct K1Smem {
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t bcnt[TH];              // border components whose root run lies in the row
+    int32_t rowfirst[TH];          // components whose root run lies in earlier rows
 };
 
 __device__ __forceinline__ int kidx(int r, int o) { return r * MAXRUN + o; }
@@ -349,9 +350,21 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // fg = byte != 0 (reading A10), one bit per pixel.  The
     // warp's S rows are all in flight before the first is used.
     uint32_t xs[S];
+    if (g.aligned && C0 + TW <= g.W && rows == TH) {  // interior tile: all 2*S loads in flight
+        const uint8_t *src = img + (int64_t)(R0 + r0) * g.W + C0 + 32 * lane;
+        uint4 v[2 * S];
 #pragma unroll
-    for (int i = 0; i < S; i++)
-        xs[i] = (r0 + i < rows && gword < g.WW) ? load_word(img, g, R0 + r0 + i, 32 * gword) : 0u;
+        for (int i = 0; i < S; i++) {
+            v[2 * i] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W));
+            v[2 * i + 1] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W + 16));
+        }
+#pragma unroll
+        for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+    } else {
+#pragma unroll
+        for (int i = 0; i < S; i++)
+            xs[i] = (r0 + i < rows && gword < g.WW) ? load_word(img, g, R0 + r0 + i, 32 * gword) : 0u;
+    }
 #pragma unroll
     for (int i = 0; i < S; i++) {
         sm.mc[r0 + i][lane] = xs[i];  // raw masks (mc is free until P2a)
@@ -473,9 +486,11 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     __syncthreads();
     if (stop <= 2) return;
     // ---- P3: flatten -- every run -> its root (Alg. flatten's p[i] <- p[p[i]],
-    // PAPER.md:711-712), own rows, lane = run ordinal.  Roots per row; a run on
-    // the tile border marks its root in bbits, and the first mark of a root
-    // counts it in its row's border-root count (row of run r = r / MAXRUN).
+    // PAPER.md:711-712), own rows, lane = run ordinal.  A root r's entry
+    // becomes 0x8000 | (its rank among the roots of its row); finds treat a
+    // flagged entry as a root.  A run on the tile border marks its root in
+    // bbits, and the first mark of a root counts it in its row's border-root
+    // count (row of run r = r / MAXRUN).
     const int lc = vcols - 1;
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
@@ -492,74 +507,85 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
                 // copied the same upper-strip run, so it is compressed too
                 const uint32_t j = vp[k];
                 uint32_t r = j;
-                while (vp[r] != r) r = vp[r];
-                vp[k] = (uint16_t)r;
-                if (j != r) vp[j] = (uint16_t)r;
+                if (!(j & 0x8000u)) {
+                    while (true) {
+                        const uint32_t v = vp[r];
+                        if (v == r || (v & 0x8000u)) break;
+                        r = v;
+                    }
+                } else {
+                    r = (uint32_t)k;  // unreachable: nobody flags another warp's runs
+                }
                 root = r == (uint32_t)k;
+                if (!root) {
+                    vp[k] = (uint16_t)r;
+                    if (j != r) vp[j] = (uint16_t)r;
+                }
                 if (edge_row || (o == 0 && lfirst) || (o == n - 1 && llast)) {
                     const uint32_t bit = 1u << (r & 31);
                     uint32_t *wd = bbits + (r / MAXRUN) * WPR + ((r % MAXRUN) >> 5);
                     if (!(atomicOr(wd, bit) & bit)) atomicAdd(&sm.bcnt[r / MAXRUN], 1);
                 }
             }
-            cnt += __popc(__ballot_sync(FULL, root));
+            const uint32_t bal = __ballot_sync(FULL, root);
+            if (root) vp[k] = (uint16_t)(0x8000u | (uint32_t)(cnt + __popc(bal & ((1u << lane) - 1u))));
+            cnt += __popc(bal);
         }
         if (lane == 0) sm.rowcnt[rl] = cnt;
     }
     __syncthreads();
     if (stop <= 3) return;
-    // ---- P3b: roots in index order = raster order of first pixels get the
+    // ---- P4: roots in index order = raster order of first pixels get the
     // consecutive component numbers (Alg. flatten's k++):
-    // component = (roots in earlier rows) + (roots before it in its row).
-    // Border roots become nodes of the global union-find in the same order;
-    // key = (image row, tile column, run ordinal): raster order.
+    // component = (roots in earlier rows) + (rank in its row).  Every run ->
+    // its component (for K5); border roots become nodes of the global
+    // union-find in index order; key = (image row, tile column, run ordinal):
+    // raster order.
     uint32_t rtot, btot;
     const int rowfirst = (int)warp_excl_scan((uint32_t)sm.rowcnt[lane], rtot);  // lane = row
     const int bfirst = (int)warp_excl_scan((uint32_t)sm.bcnt[lane], btot);
     const int ncomp = (int)rtot, nborder = (int)btot;
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
-#pragma unroll 1
-    for (int i = 0; i < S; i++) {
-        const int rl = r0 + i, n = sm.nrun[rl];
-        int c = __shfl_sync(FULL, rowfirst, rl), bi = __shfl_sync(FULL, bfirst, rl);
-        const uint32_t *brow = bbits + rl * WPR;
-#pragma unroll 1
-        for (int o0 = 0; o0 < n; o0 += 32) {
-            const int o = o0 + lane, k = kidx(rl, o);
-            const bool root = o < n && vp[k] == (uint32_t)k;
-            const bool broot = root && ((brow[o >> 5] >> (o & 31)) & 1u);
-            const uint32_t bal = __ballot_sync(FULL, root), bbal = __ballot_sync(FULL, broot);
-            const uint32_t lt = (1u << lane) - 1u;
-            if (root) {
-                const int ci = c + __popc(bal & lt);
-                vp[k] = (uint16_t)(0x8000u | (uint32_t)ci);
-                if (broot) {
-                    const int node = nodebase + bi + __popc(bbal & lt);
-                    compnode[ci] = node;
-                    ws.gparent[node] = node;
-                    ws.gnodecomp[node] = (rl << 16) | ci;
-                    ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
-                }
-            }
-            c += __popc(bal);
-            bi += __popc(bbal);
-        }
-    }
-    __syncthreads();
-    if (stop <= 4) return;
-    auto comp_of = [&](int k) -> int {
+    if (w == 0) sm.rowfirst[lane] = rowfirst;
+    auto comp_of = [&](int k) -> int {  // after the barrier below
         const uint32_t pk = sm.p[k];
-        return (int)((pk & 0x8000u) ? (pk & 0x3FFFu) : (sm.p[pk] & 0x3FFFu));
+        const int r = (pk & 0x8000u) ? k : (int)pk;
+        const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
+        return sm.rowfirst[r / MAXRUN] + (int)(pr & 0x1FFu);
     };
-    // ---- P4a: component of every run (for K5)
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
+        const int rf = __shfl_sync(FULL, rowfirst, rl);
+        int bi = __shfl_sync(FULL, bfirst, rl);
+        const bool hasb = sm.bcnt[rl] != 0;
+        const uint32_t *brow = bbits + rl * WPR;
 #pragma unroll 1
-        for (int o = lane; o < n; o += 32) dst[o] = (uint16_t)comp_of(kidx(rl, o));
+        for (int o0 = 0; o0 < n; o0 += 32) {
+            const int o = o0 + lane, k = kidx(rl, o);
+            const uint32_t pk = o < n ? sm.p[k] : 0u;
+            const int r = (pk & 0x8000u) ? k : (int)pk;
+            const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
+            const int c = __shfl_sync(FULL, rowfirst, r / MAXRUN) + (int)(pr & 0x1FFu);
+            if (o < n) dst[o] = (uint16_t)c;
+            if (hasb) {
+                const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
+                const uint32_t bbal = __ballot_sync(FULL, broot);
+                if (broot) {
+                    const int node = nodebase + bi + __popc(bbal & ((1u << lane) - 1u));
+                    compnode[c] = node;
+                    ws.gparent[node] = node;
+                    ws.gnodecomp[node] = (rl << 16) | c;
+                    ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
+                }
+                bi += __popc(bbal);
+            }
+        }
     }
+    __syncthreads();
+    if (stop <= 4) return;
     // ---- P4c: nodes of the border pixels (for K2)
     {
         const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
