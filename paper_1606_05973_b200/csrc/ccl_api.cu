@@ -30,7 +30,7 @@ Geometry make_geometry(int H, int W) {
 }
 
 enum {
-    A_BM, A_FM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
+    A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
     A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_COUNT
 };
 
@@ -38,7 +38,6 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
     const size_t nT = (size_t)g.nT, H = (size_t)g.H;
     const size_t sz[A_COUNT] = {
         H * g.WW * 4,                   // bm
-        H * g.WW * 4,                   // fm
         H * g.nTx * g.maxrun * 2,       // runcomp
         nT * g.capc * 4,                // compnode
         nT * g.capc * 4,                // complab
@@ -70,7 +69,6 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     char *b = static_cast<char *>(base);
     Workspace w;
     w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
-    w.fm = reinterpret_cast<uint32_t *>(b + offs[A_FM]);
     w.runcomp = reinterpret_cast<uint16_t *>(b + offs[A_RUNCOMP]);
     w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);
     w.complab = reinterpret_cast<int32_t *>(b + offs[A_COMPLAB]);

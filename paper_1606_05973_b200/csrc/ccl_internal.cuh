@@ -41,7 +41,6 @@ struct Geometry {
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
-    uint32_t *fm;         // [H][WW]           bm with bridged single-pixel holes set (run mask)
     uint16_t *runcomp;    // [H][nTx][maxrun]  tile component of each run of each tile row
     int32_t *compnode;    // [nT][capc]        border-node id of a border component (others unset)
     int32_t *complab;     // [nT][capc]        band-local label of the component (1..N_band)

@@ -258,6 +258,27 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
     return load_word_bytes(src, min(32, g.W - col0));
 }
 
+// Run mask of image row `row`, word `gword` (lane = word within the tile
+// column; whole warp): the foreground with the tile-local bridged single-pixel
+// holes filled, exactly as K1 P0b fills them (holes whose left/right
+// neighbours are in the tile, bridged by the pixel above or below inside the
+// tile).  *fg receives the foreground word itself.
+__device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *__restrict__ bm,
+                                             int row, int gword, uint32_t *fg) {
+    const int lane = lane_id();
+    const int R0 = (row / TH) * TH, rl = row - R0, rows = min(TH, g.H - R0);
+    const bool ok = gword < g.WW;
+    const int64_t i = (int64_t)row * g.WW + gword;
+    const uint32_t x0 = ok ? __ldcg(bm + i) : 0u;
+    const uint32_t u = (ok && rl > 0) ? __ldcg(bm + i - g.WW) : 0u;
+    const uint32_t d = (ok && rl + 1 < rows) ? __ldcg(bm + i + g.WW) : 0u;
+    const uint32_t xlr = __shfl_up_sync(FULL, x0, 1), xrr = __shfl_down_sync(FULL, x0, 1);
+    const uint32_t xl = lane == 0 ? 0u : xlr, xr = lane == 31 ? 0u : xrr;
+    const uint32_t holes = ~x0 & ((x0 << 1) | (xl >> 31)) & ((x0 >> 1) | (xr << 31));
+    if (fg) *fg = x0;
+    return x0 | (holes & (u | d));
+}
+
 // ========================================================================= K1
 // Tile-local two-pass labeling with runs as the provisional labels.  The run
 // with ordinal o in tile row r has index k = r*MAXRUN + o; indices grow in
@@ -390,7 +411,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         const uint32_t d = rl + 1 < rows ? sm.mc[rl + 1][lane] : 0u;
         const uint32_t holes = ~x0 & ((x0 << 1) | (xl >> 31)) & ((x0 >> 1) | (xr << 31));
         const uint32_t x = x0 | (holes & (u | d));
-        if (rl < rows && gword < g.WW) ws.fm[(int64_t)(R0 + rl) * g.WW + gword] = x;
         const uint32_t xfl = __shfl_up_sync(FULL, x, 1);
         const uint32_t hx = x & ~((x << 1) | (lane == 0 ? 0u : (xfl >> 31)));
         uint32_t nr;
@@ -625,8 +645,8 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
         const int ru = ty * TH - 1, rx = ty * TH;
         const int gword = tx * WPR + lane;
-        const uint32_t u = gword < g.WW ? ws.fm[(int64_t)ru * g.WW + gword] : 0u;
-        const uint32_t x = gword < g.WW ? ws.fm[(int64_t)rx * g.WW + gword] : 0u;
+        const uint32_t u = run_mask(g, ws.bm, ru, gword, nullptr);
+        const uint32_t x = run_mask(g, ws.bm, rx, gword, nullptr);
         RowView U = make_row(u), X = make_row(x);
         shd[wib][0][lane] = U.hx; sbs[wib][0][lane] = U.base;
         shd[wib][1][lane] = X.hx; sbs[wib][1][lane] = X.base;
@@ -650,7 +670,7 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             const uint32_t s = smear_up(t, x);
             const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
             const uint32_t S_ = s | (cin ? (x & ~(x + 1)) : 0u);
-            const uint32_t d = gword < g.WW ? ws.fm[(int64_t)(ru - 1) * g.WW + gword] : 0u;
+            const uint32_t d = run_mask(g, ws.bm, ru - 1, gword, nullptr);
             m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_) & ~hole_bridged(u, U.xp, d);
         }
         while (m) {
@@ -890,14 +910,16 @@ __global__ void __launch_bounds__(K5_WARPS * 32, 8)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
     __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
     const int lane = lane_id(), wi = threadIdx.x >> 5;
-    const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
-    if (seg >= g.nseg) return;
-    const int row = (int)(seg / g.nTx), tx = (int)(seg % g.nTx);
+    // CTA = K5_WARPS consecutive rows of one tile column (they share bm rows
+    // and the tile's component labels in L1); warp = one row segment
+    const int tx = blockIdx.x % g.nTx, row = (blockIdx.x / g.nTx) * K5_WARPS + wi;
+    if (row >= g.H) return;
+    const int64_t seg = (int64_t)row * g.nTx + tx;  // (row, tile column)
     const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
-    const uint32_t f = gword < g.WW ? __ldcg(ws.fm + (int64_t)row * g.WW + gword) : 0u;  // runs
-    const uint32_t x = gword < g.WW ? __ldcg(ws.bm + (int64_t)row * g.WW + gword) : 0u;  // foreground
+    uint32_t x;                                          // foreground
+    const uint32_t f = run_mask(g, ws.bm, row, gword, &x);  // runs
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
@@ -950,8 +972,8 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     if (tx >= g.nTx) return;
     const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int gword = tx * WPR + lane;
-    const uint32_t f = gword < g.WW ? ws.fm[(int64_t)row * g.WW + gword] : 0u;
-    const uint32_t x = gword < g.WW ? ws.bm[(int64_t)row * g.WW + gword] : 0u;
+    uint32_t x;
+    const uint32_t f = run_mask(g, ws.bm, row, gword, &x);
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
@@ -1045,7 +1067,7 @@ cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *lab
     mark(K_FIXUP);
     k_fixup<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws, boff);
     mark(K_WRITE);
-    k_write<<<(unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream>>>(g, ws, labels, boff);
+    k_write<<<(unsigned)((int64_t)((g.H + K5_WARPS - 1) / K5_WARPS) * g.nTx), K5_WARPS * 32, 0, stream>>>(g, ws, labels, boff);
     mark(K_COUNT);
     return cudaGetLastError();
 }
