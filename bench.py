@@ -29,7 +29,7 @@ WORKLOAD = "c4_voronoi_21600"
 # algorithmic bytes per pixel: 1 B image read + 4 B label write
 # (k_tile_local reads the image, k_write writes the labels; the rest move intermediates)
 ALG_BYTES_PER_PX = {"path": 5, "k_tile_local": 1, "k_write": 4,
-                    "k_border": 0, "k_number": 0, "k_fixup": 0}
+                    "k_border": 0, "k_number": 0, "k_label": 0, "k_fixup": 0}
 
 
 def parse_args():
@@ -208,7 +208,7 @@ def main():
         step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
         nTx, nTy = (W + 1023) // 1024, (H + 31) // 32
         # mirrors cclb::pipeline_launches: k_border only runs when tiles have neighbours
-        launches_per_step = 4 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
+        launches_per_step = 5 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
     else:
         uid = ccl.nccl_unique_id() if rank == 0 else None
         obj = [uid]

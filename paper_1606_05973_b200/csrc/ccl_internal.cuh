@@ -44,6 +44,7 @@ struct Workspace {
     uint16_t *runcomp;    // [H][nTx][maxrun]  tile component of each run of each tile row
     int32_t *compnode;    // [nT][capc]        border-node id of a border component (others unset)
     int32_t *complab;     // [nT][capc]        band-local label of the component (1..N_band)
+    uint8_t *comprow;     // [nT][capc]        tile row of the component's root run
     int32_t *gparent;     // [nT][capb]        global union-find over border components
     int64_t *gkey;        // [nT][capb]        (image row, tile column, run ordinal) key: raster order
     int32_t *gnodecomp;   // [nT][capb]        (root row in tile << 16) | tile component of the node
@@ -57,6 +58,7 @@ struct Workspace {
     int32_t *segoff;      // [nseg]            exclusive prefix of segcnt inside its tile row
     unsigned long long *scanstate;  // [nTy]   decoupled-lookback descriptors (one per tile row)
     int32_t *ticket;      // [1]               dynamic partition counter
+    int32_t *rowexcl;     // [nTy]             labels of earlier tile rows
     // row bands only (null for a whole image):
     const int32_t *xlab;  // [*]               labels of roots owned by other bands; a node
                           //                   whose parent is -2-f takes xlab[f]
@@ -67,7 +69,8 @@ Geometry make_geometry(int H, int W);
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 
-enum { K_TILE = 0, K_BORDER, K_NUMBER, K_FIXUP, K_WRITE, K_COUNT };
+
+enum { K_TILE = 0, K_BORDER, K_NUMBER, K_LABEL, K_FIXUP, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it

@@ -34,8 +34,8 @@ namespace cclb {
 
 #define FULL 0xFFFFFFFFu
 
-const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number", "k_fixup",
-                                           "k_write"};
+const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number", "k_label",
+                                           "k_fixup", "k_write"};
 
 // ===================================================================== helpers
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -566,6 +566,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     const int bfirst = (int)warp_excl_scan((uint32_t)sm.bcnt[lane], btot);
     const int ncomp = (int)rtot, nborder = (int)btot;
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
+    uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
     if (w == 0) sm.rowfirst[lane] = rowfirst;
     auto comp_of = [&](int k) -> int {  // after the barrier below
@@ -589,7 +590,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             const int r = (pk & 0x8000u) ? k : (int)pk;
             const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
             const int c = __shfl_sync(FULL, rowfirst, r / MAXRUN) + (int)(pr & 0x1FFu);
-            if (o < n) dst[o] = (uint16_t)c;
+            if (o < n) {
+                dst[o] = (uint16_t)c;
+                if (pk & 0x8000u) comprow[c] = (uint8_t)rl;
+            }
             if (hasb) {
                 const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
                 const uint32_t bbal = __ballot_sync(FULL, broot);
@@ -684,21 +688,39 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         }
         return;
     }
-    // vertical edges
+    // vertical edges; lanes = consecutive rows of one edge, and a union that
+    // the row above already made (same pair of nodes) is skipped -- a region
+    // crossing the edge repeats its pair on every row it spans
     const int64_t t = (int64_t)(gw - nh_warps) * 32 + lane;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    if (t >= nv) return;
-    const int tx = 1 + (int)(t / g.H), r = (int)(t % g.H);
-    const int a = ws.rightnode[(int64_t)(tx - 1) * g.H + r];
+    int tx = 0, r = 0, a = -1, b = -1;
+    const int32_t *L = nullptr;
+    if (t < nv) {
+        tx = 1 + (int)(t / g.H);
+        r = (int)(t % g.H);
+        a = ws.rightnode[(int64_t)(tx - 1) * g.H + r];
+        L = ws.leftnode + (int64_t)tx * g.H;
+        if (a >= 0) b = L[r];
+    }
+    const int ap = __shfl_up_sync(FULL, a, 1), bp = __shfl_up_sync(FULL, b, 1);
+    const int an = __shfl_down_sync(FULL, a, 1), bn = __shfl_down_sync(FULL, b, 1);
+    const bool up_ok = lane > 0 && r > 0;         // lane-1 is row r-1 of this edge
+    const bool dn_ok = lane < 31 && r + 1 < g.H;  // lane+1 is row r+1 of this edge
     if (a < 0) return;
-    const int32_t *L = ws.leftnode + (int64_t)tx * g.H;
-    const int b = L[r];
     if (b >= 0) {
-        gunion(ws.gparent, ws.gkey, a, b);  // (r-1) and (r+1) are then joined through b
+        // (r-1) and (r+1) are then joined through b
+        if (!(up_ok && ap == a && bp == b)) gunion(ws.gparent, ws.gkey, a, b);
         return;
     }
-    if (r > 0 && L[r - 1] >= 0) gunion(ws.gparent, ws.gkey, a, L[r - 1]);
-    if (r + 1 < g.H && L[r + 1] >= 0) gunion(ws.gparent, ws.gkey, a, L[r + 1]);
+    // diagonal neighbours; skipped when the adjacent row makes the same union
+    if (r > 0) {
+        const int bu = L[r - 1];
+        if (bu >= 0 && !(up_ok && ap == a && bp == bu)) gunion(ws.gparent, ws.gkey, a, bu);
+    }
+    if (r + 1 < g.H) {
+        const int bd = L[r + 1];
+        if (bd >= 0 && !(dn_ok && an == a && bn == bd)) gunion(ws.gparent, ws.gkey, a, bd);
+    }
 }
 
 // ========================================================================= K3
@@ -714,11 +736,7 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
 // lookback, and every root gets  offset(segment) + rank in segment + 1:
 // flatten's consecutive numbering k++  made canonical.
 struct KNSmem {
-    uint32_t nrbits[KN_WARPS][CAPC / 32];  // non-root border components of the warp's tile
-    int32_t wpre[KN_WARPS][CAPC / 32];     // exclusive popcount prefix of nrbits
-    int32_t rowfirst[KN_WARPS][TH + 1];
-    int32_t nrrow[KN_WARPS][TH];           // non-roots per row, then their exclusive prefix
-    int32_t rbase[KN_WARPS][TH];           // label of the row's first root minus its index
+    int32_t nrrow[KN_WARPS][TH];           // non-root border components per row
     int32_t wsum[KN_WARPS];
     int32_t part, excl;
 };
@@ -755,7 +773,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         const int tile = ty * g.nTx + tx;
         const int32_t *meta = ws.meta + (int64_t)tile * META;
         const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
-        kn_nonroots(ws, tile * g.capb, nborder, sm.nrbits[w], 0, sm.nrrow[w], false);
+        kn_nonroots(ws, tile * g.capb, nborder, nullptr, 0, sm.nrrow[w], false);
         const int rf = __ldcg(meta + META_ROWFIRST + lane);
         const int rfn = lane + 1 < rows ? __ldcg(meta + META_ROWFIRST + lane + 1) : ncomp;
         if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = rfn - rf - sm.nrrow[w][lane];
@@ -828,54 +846,79 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     __syncthreads();
-    const int excl = sm.excl;
-    // ---- phase 3: labels of the roots (components and border nodes)
-    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
-        const int tile = ty * g.nTx + tx;
-        const int32_t *meta = ws.meta + (int64_t)tile * META;
-        const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
-        const int nbw = (ncomp + 31) >> 5;
-        uint32_t *bits = sm.nrbits[w];
-        int32_t *wpre = sm.wpre[w], *rf = sm.rowfirst[w], *rb = sm.rbase[w];
-        const int nodebase = tile * g.capb;
-        kn_nonroots(ws, nodebase, nborder, bits, nbw, sm.nrrow[w], true);
-        for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
-            const int j = j0 + lane;
-            const uint32_t pc = j < nbw ? __popc(bits[j]) : 0u;
-            uint32_t tot;
-            const int pre = (int)warp_excl_scan(pc, tot);
-            if (j < nbw) wpre[j] = acc + pre;
-            acc += (int)tot;
+    if (threadIdx.x == 0) ws.rowexcl[ty] = sm.excl;
+}
+
+// ======================================================================== K3b
+// One warp per tile: labels of the tile's global roots (components and
+// border nodes):  offset(segment) + rank in segment + 1, where the rank of a
+// root among the roots of its segment is its component index minus the
+// components of earlier rows minus the non-root border components before it.
+constexpr int KL_WARPS = 8;
+struct KLSmem {
+    uint32_t nrbits[KL_WARPS][CAPC / 32];  // non-root border components of the warp's tile
+    uint16_t wpre[KL_WARPS][CAPC / 32];    // exclusive popcount prefix of nrbits
+    int32_t nrrow[KL_WARPS][TH];           // non-roots per row
+    int32_t rbase[KL_WARPS][TH];           // label of the row's first root minus its index
+};
+
+__global__ void __launch_bounds__(KL_WARPS * 32)
+k_label(Geometry g, Workspace ws) {
+    __shared__ KLSmem sm;
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int tile = blockIdx.x * KL_WARPS + w;
+    if (tile >= g.nT) return;
+    const int tx = tile % g.nTx, ty = tile / g.nTx;
+    const int R0 = ty * TH, rows = min(TH, g.H - R0);
+    const int32_t *meta = ws.meta + (int64_t)tile * META;
+    const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
+    const int f = __ldcg(meta + META_ROWFIRST + lane);
+    const int so = lane < rows ? __ldcg(ws.segoff + (int64_t)(R0 + lane) * g.nTx + tx) : 0;
+    const int excl = __ldcg(ws.rowexcl + ty);
+    const int nbw = (ncomp + 31) >> 5;
+    uint32_t *bits = sm.nrbits[w];
+    uint16_t *wpre = sm.wpre[w];
+    int32_t *rb = sm.rbase[w];
+    const int nodebase = tile * g.capb;
+    kn_nonroots(ws, nodebase, nborder, bits, nbw, sm.nrrow[w], true);
+    for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
+        const int j = j0 + lane;
+        const uint32_t pc = j < nbw ? __popc(bits[j]) : 0u;
+        uint32_t tot;
+        const int pre = (int)warp_excl_scan(pc, tot);
+        if (j < nbw) wpre[j] = (uint16_t)(acc + pre);
+        acc += (int)tot;
+    }
+    {
+        uint32_t tot;
+        const int nrp = (int)warp_excl_scan((uint32_t)sm.nrrow[w][lane], tot);
+        // label(c) = excl + segoff + (roots before c in the tile) - (roots
+        // in earlier rows) + 1, roots before c = c - nonroots before c
+        rb[lane] = excl + so - (f - nrp) + 1;
+    }
+    __syncwarp();
+    auto nonroots_before = [&](int c) -> int {
+        return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
+    };
+    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+    const uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
+    // four components per lane in flight
+    for (int c0 = lane; c0 < ncomp; c0 += 128) {
+        uint32_t rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) rr[u] = c0 + 32 * u < ncomp ? __ldcg(comprow + c0 + 32 * u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int c = c0 + 32 * u;
+            if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
+            complab[c] = rb[rr[u]] + c - nonroots_before(c);
         }
-        {
-            uint32_t tot;
-            const int nrp = (int)warp_excl_scan((uint32_t)sm.nrrow[w][lane], tot);
-            const int f = __ldcg(meta + META_ROWFIRST + lane);
-            rf[lane] = f;
-            if (lane == 0) rf[TH] = ncomp;
-            const int so = lane < rows ? __ldcg(ws.segoff + sbase + (int64_t)lane * g.nTx + tx) : 0;
-            // label(c) = excl + segoff + (roots before c in the tile) - (roots
-            // in earlier rows) + 1, roots before c = c - nonroots before c
-            rb[lane] = excl + so - (f - nrp) + 1;
-        }
-        __syncwarp();
-        auto nonroots_before = [&](int c) -> int {
-            return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
-        };
-        int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-        int r = 0;  // row of component c: components are in row order, so it only grows
-        for (int c = lane; c < ncomp; c += 32) {
-            while (r + 1 < rows && rf[r + 1] <= c) r++;
-            if ((bits[c >> 5] >> (c & 31)) & 1u) continue;  // K4 writes it
-            complab[c] = rb[r] + c - nonroots_before(c);
-        }
-        for (int j = lane; j < nborder; j += 32) {
-            const int node = nodebase + j;
-            if (__ldcg(ws.gparent + node) != node) continue;
-            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
-            ws.gnodelab[node] = rb[gc >> 16] + c - nonroots_before(c);
-        }
-        __syncwarp();
+    }
+    for (int j = lane; j < nborder; j += 32) {
+        const int node = nodebase + j;
+        if (__ldcg(ws.gparent + node) != node) continue;
+        const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
+        ws.gnodelab[node] = rb[gc >> 16] + c - nonroots_before(c);
     }
 }
 
@@ -1014,7 +1057,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 4 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
@@ -1056,6 +1099,8 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
                             cudaStream_t stream, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[K_NUMBER], stream);
     k_number<<<g.nTy, KN_WARPS * 32, 0, stream>>>(g, ws, n_components);
+    if (ev) cudaEventRecord(ev[K_LABEL], stream);
+    k_label<<<(g.nT + KL_WARPS - 1) / KL_WARPS, KL_WARPS * 32, 0, stream>>>(g, ws);
     return cudaGetLastError();
 }
 
