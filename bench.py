@@ -224,8 +224,6 @@ def main():
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-    if plan is not None:
-        plan.set_profiling(args.steps)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     if dist:
@@ -250,6 +248,14 @@ def main():
     peak, peak_src = peak_hbm()
     roofline = None
     if plan is not None:
+        # Per-kernel times: the same K steps again with CUDA events recorded on
+        # the launch stream between the kernels.  Kept out of the timed region
+        # above because events between kernels serialise the programmatic
+        # dependent launches the pipeline uses.
+        plan.set_profiling(args.steps)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize(dev)
         ktimes = plan.kernel_times()
         plan.set_profiling(0)
         # The path is HBM-bound by its algorithmic bytes (SURVEY.md section 8(d):

@@ -38,6 +38,13 @@ const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number
                                            "k_fixup", "k_write"};
 
 // ===================================================================== helpers
+// Programmatic dependent launch: a kernel waits for its predecessor's grid to
+// complete (memory visible) before touching what it wrote, and lets its
+// successor be scheduled once each of its CTAs has issued its last store, so
+// the launch gaps between the pipeline's kernels overlap the tails.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // bits 0..b set
@@ -333,6 +340,7 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
 
 __global__ void __launch_bounds__(NW * 32, 5)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
+    pdl_trigger();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
 
@@ -347,10 +355,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     volatile uint16_t *vp = sm.p;
     uint32_t *bbits = &sm.mc[0][0];
 
-    if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
-        for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
-        if (threadIdx.x == 0) *ws.ticket = 0;
-    }
     // Warm L2 with the pixels of the tile that will start about one wave of
     // resident CTAs later (pfd = resident CTAs on the device): its loads then
     // hit L2 instead of waiting on HBM.
@@ -385,6 +389,11 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
 #pragma unroll
         for (int i = 0; i < S; i++)
             xs[i] = (r0 + i < rows && gword < g.WW) ? load_word(img, g, R0 + r0 + i, 32 * gword) : 0u;
+    }
+    pdl_wait();  // the previous call's kernels are done with the workspace
+    if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
+        for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
+        if (threadIdx.x == 0) *ws.ticket = 0;
     }
 #pragma unroll
     for (int i = 0; i < S; i++) {
@@ -642,6 +651,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
 // corner pixels): one thread per (tile column boundary, row).
 __global__ void __launch_bounds__(256)
 k_border(Geometry g, Workspace ws, int nh_warps) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ uint32_t shd[8][2][WPR], sbs[8][2][WPR];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * 8 + wib;
@@ -762,6 +773,8 @@ __device__ __forceinline__ void kn_nonroots(const Workspace &ws, int nodebase, i
 
 __global__ void __launch_bounds__(KN_WARPS * 32, 6)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ KNSmem sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
@@ -864,6 +877,8 @@ struct KLSmem {
 
 __global__ void __launch_bounds__(KL_WARPS * 32)
 k_label(Geometry g, Workspace ws) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ KLSmem sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int tile = blockIdx.x * KL_WARPS + w;
@@ -929,6 +944,8 @@ k_label(Geometry g, Workspace ws) {
 // K5 adds the band offset).  One warp per tile, over its border nodes.
 __global__ void __launch_bounds__(256)
 k_fixup(Geometry g, Workspace ws, int32_t boff) {
+    pdl_trigger();
+    pdl_wait();
     const int lane = lane_id();
     const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (tile >= g.nT) return;
@@ -951,6 +968,8 @@ k_fixup(Geometry g, Workspace ws, int32_t boff) {
 constexpr int K5_WARPS = 8;
 __global__ void __launch_bounds__(K5_WARPS * 32, 8)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
     const int lane = lane_id(), wi = threadIdx.x >> 5;
     // CTA = K5_WARPS consecutive rows of one tile column (they share bm rows
@@ -1060,6 +1079,23 @@ int pipeline_launches(const Geometry &g) {
     return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
 }
 
+// Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
@@ -1085,22 +1121,27 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    k_tile_local<<<g.nT, NW * 32, (int)sizeof(K1Smem), stream>>>(img, g, ws, g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
+    e = launch_pdl(k_tile_local, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws,
+                   g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
+    if (e != cudaSuccess) return e;
     mark(K_BORDER);
     if (g_k1_stop < 99) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
     const int64_t warps = nh + (nv + 31) / 32;
-    if (warps > 0) k_border<<<(unsigned)((warps + 7) / 8), 256, 0, stream>>>(g, ws, nh);
+    if (warps > 0) e = launch_pdl(k_border, (unsigned)((warps + 7) / 8), 256, 0, stream, g, ws, nh);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[K_NUMBER], stream);
-    k_number<<<g.nTy, KN_WARPS * 32, 0, stream>>>(g, ws, n_components);
+    cudaError_t e = launch_pdl(k_number, g.nTy, KN_WARPS * 32, 0, stream, g, ws, n_components);
+    if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[K_LABEL], stream);
-    k_label<<<(g.nT + KL_WARPS - 1) / KL_WARPS, KL_WARPS * 32, 0, stream>>>(g, ws);
+    e = launch_pdl(k_label, (g.nT + KL_WARPS - 1) / KL_WARPS, KL_WARPS * 32, 0, stream, g, ws);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -1110,9 +1151,12 @@ cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *lab
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_FIXUP);
-    k_fixup<<<(g.nT + 7) / 8, 256, 0, stream>>>(g, ws, boff);
+    cudaError_t e = launch_pdl(k_fixup, (g.nT + 7) / 8, 256, 0, stream, g, ws, boff);
+    if (e != cudaSuccess) return e;
     mark(K_WRITE);
-    k_write<<<(unsigned)((int64_t)((g.H + K5_WARPS - 1) / K5_WARPS) * g.nTx), K5_WARPS * 32, 0, stream>>>(g, ws, labels, boff);
+    e = launch_pdl(k_write, (unsigned)((int64_t)((g.H + K5_WARPS - 1) / K5_WARPS) * g.nTx), K5_WARPS * 32, 0,
+                   stream, g, ws, labels, boff);
+    if (e != cudaSuccess) return e;
     mark(K_COUNT);
     return cudaGetLastError();
 }
