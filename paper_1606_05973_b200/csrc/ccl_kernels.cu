@@ -439,7 +439,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // own rows in order, so inside a strip a run copies its upper neighbour's
     // parent (already final within the strip); a strip's first row copies the
     // upper run's index (a run of the strip above).
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         if (rl >= rows || rl == 0) {
@@ -491,7 +491,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // (the decision tree's copy(c,a)/copy(c,d) merges).  The
     // parent chains may still cross strips (a strip's first row points into
     // the strip above): Rem's algorithm works on any forest with p[x] <= x.
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
         uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
