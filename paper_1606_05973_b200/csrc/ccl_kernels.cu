@@ -972,14 +972,19 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
     pdl_wait();
     __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
     const int lane = lane_id(), wi = threadIdx.x >> 5;
-    // CTA = K5_WARPS consecutive rows of one tile column (they share bm rows
-    // and the tile's component labels in L1); warp = one row segment
-    const int tx = blockIdx.x % g.nTx, row = (blockIdx.x / g.nTx) * K5_WARPS + wi;
-    if (row >= g.H) return;
-    const int64_t seg = (int64_t)row * g.nTx + tx;  // (row, tile column)
+    // warp = one row segment; consecutive warps and CTAs take consecutive
+    // segments in raster order, so the stores in flight cover one contiguous
+    // stretch of the label image
+    const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
+    if (seg >= g.nseg) return;
+    const int row = (int)(seg / g.nTx), tx = (int)(seg % g.nTx);
     const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
+    const uint16_t *rc = ws.runcomp + seg * g.maxrun;
+    // the first 32 run -> component entries are loaded beside the masks (most
+    // rows have fewer runs), so the label gather is the only dependent load
+    const uint32_t rc0 = lane < g.maxrun ? (uint32_t)__ldcs(rc + lane) : 0u;
     uint32_t x;                                          // foreground
     const uint32_t f = run_mask(g, ws.bm, row, gword, &x);  // runs
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
@@ -988,10 +993,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     int32_t *rowlab = s_lab[wi];
     {
-        const uint16_t *rc = ws.runcomp + seg * g.maxrun;
         const int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+        if (lane < (int)nr) rowlab[lane] = complab[rc0] + off;
 #pragma unroll 1
-        for (int k = lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)] + off;
+        for (int k = 32 + lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)] + off;
     }
     __syncwarp();
     int32_t *out = labels + (int64_t)row * g.W + C0;
@@ -1014,7 +1019,7 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
         int v3 = (nib & 8u) ? L : 0;
         const int P = 128 * c + 4 * lane;
         if (g.aligned) {
-            if (P < vcols) __stcs(reinterpret_cast<int4 *>(out + P), make_int4(v0, v1, v2, v3));
+            if (P < vcols) *reinterpret_cast<int4 *>(out + P) = make_int4(v0, v1, v2, v3);
         } else {
             if (P < vcols) __stcs(out + P, v0);
             if (P + 1 < vcols) __stcs(out + P + 1, v1);
@@ -1154,7 +1159,7 @@ cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *lab
     cudaError_t e = launch_pdl(k_fixup, (g.nT + 7) / 8, 256, 0, stream, g, ws, boff);
     if (e != cudaSuccess) return e;
     mark(K_WRITE);
-    e = launch_pdl(k_write, (unsigned)((int64_t)((g.H + K5_WARPS - 1) / K5_WARPS) * g.nTx), K5_WARPS * 32, 0,
+    e = launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0,
                    stream, g, ws, labels, boff);
     if (e != cudaSuccess) return e;
     mark(K_COUNT);
