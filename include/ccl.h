@@ -77,6 +77,17 @@ ccl_status ccl_label(const uint8_t *img, int H, int W, int32_t *labels,
                      int32_t *n_components, ccl_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * ccl_label_threshold -- ccl_label on a grayscale image thresholded on load:
+ * pixel (r,c) is foreground <=> img[r*W + c] > threshold (0..255; 0 gives
+ * ccl_label's byte != 0).  This is the paper's im2bw preprocessing fused into
+ * the pixel read ("converted to binary ... level 0.5";
+ * for 8-bit images level 0.5 is threshold 127: gray >= 128).
+ * section 8(f) row f1.  threshold outside 0..255 -> CCL_INVALID_ARGUMENT.
+ * ---------------------------------------------------------------------- */
+ccl_status ccl_label_threshold(const uint8_t *img, int H, int W, int threshold, int32_t *labels,
+                               int32_t *n_components, ccl_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Plans: preallocate the workspace for one image shape once, then label many
  * images of that shape with no allocation.  A plan may be used by one stream
  * at a time.
@@ -86,6 +97,9 @@ typedef struct ccl_plan_st *ccl_plan;
 /* Allocates device workspace for H x W images on the current device. */
 ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out);
 ccl_status ccl_plan_destroy(ccl_plan plan);
+/* Foreground <=> byte > threshold for the plan's later calls (0..255; the
+ * default 0 is byte != 0).  See ccl_label_threshold. */
+ccl_status ccl_plan_set_threshold(ccl_plan plan, int threshold);
 /* Bytes of device workspace the plan holds. */
 ccl_status ccl_plan_workspace_bytes(ccl_plan plan, uint64_t *bytes);
 

@@ -31,6 +31,10 @@ _L.ccl_version.argtypes = []
 _L.ccl_version.restype = ctypes.c_char_p
 _L.ccl_label.argtypes = [_vp, _i, _i, _vp, _vp, _vp]
 _L.ccl_label.restype = _i
+_L.ccl_label_threshold.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
+_L.ccl_label_threshold.restype = _i
+_L.ccl_plan_set_threshold.argtypes = [_vp, _i]
+_L.ccl_plan_set_threshold.restype = _i
 _L.ccl_plan_create.argtypes = [_i, _i, ctypes.POINTER(_vp)]
 _L.ccl_plan_create.restype = _i
 _L.ccl_plan_destroy.argtypes = [_vp]
@@ -99,8 +103,9 @@ def _check_img(img):
         raise ValueError("img must be contiguous (pitch == W)")
 
 
-def label(img, out=None, n_out=None, stream=None):
-    """Labels a 2-D uint8 CUDA image (foreground <=> != 0) with 8-connectivity.
+def label(img, out=None, n_out=None, stream=None, threshold=None):
+    """Labels a 2-D uint8 CUDA image (foreground <=> != 0, or > `threshold`
+    when given: ccl_label_threshold) with 8-connectivity.
     Returns (labels int32 HxW on the same device, n_components int32 tensor [1]).
     Labels are 1..N in raster order of each component's first pixel, 0 = background.
     Asynchronous on `stream` (default: current stream)."""
@@ -110,8 +115,12 @@ def label(img, out=None, n_out=None, stream=None):
         out = torch.empty((H, W), dtype=torch.int32, device=img.device)
     if n_out is None:
         n_out = torch.empty(1, dtype=torch.int32, device=img.device)
-    _check(_L.ccl_label(img.data_ptr(), H, W, out.data_ptr(), n_out.data_ptr(),
-                        _stream_handle(stream)), "ccl_label")
+    if threshold is None:
+        _check(_L.ccl_label(img.data_ptr(), H, W, out.data_ptr(), n_out.data_ptr(),
+                            _stream_handle(stream)), "ccl_label")
+    else:
+        _check(_L.ccl_label_threshold(img.data_ptr(), H, W, int(threshold), out.data_ptr(), n_out.data_ptr(),
+                                      _stream_handle(stream)), "ccl_label_threshold")
     return out, n_out
 
 
@@ -124,6 +133,10 @@ class Plan:
         self._p = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _check(_L.ccl_plan_create(self.H, self.W, ctypes.byref(self._p)), "ccl_plan_create")
+
+    def set_threshold(self, threshold):
+        """Foreground <=> byte > threshold for later label() calls (0 = byte != 0)."""
+        _check(_L.ccl_plan_set_threshold(self._p, int(threshold)), "ccl_plan_set_threshold")
 
     def workspace_bytes(self):
         b = ctypes.c_uint64()

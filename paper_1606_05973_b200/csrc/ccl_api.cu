@@ -26,6 +26,7 @@ Geometry make_geometry(int H, int W) {
     g.capb = 2 * g.maxrun + th;
     g.aligned = (W % 16) == 0;
     g.row0 = 0;
+    g.thr = 0;
     return g;
 }
 
@@ -154,11 +155,18 @@ const char *ccl_version(void) { return "0.1.0"; }
 
 ccl_status ccl_label(const uint8_t *img, int H, int W, int32_t *labels, int32_t *n_components,
                      ccl_stream_t stream) {
+    return ccl_label_threshold(img, H, W, 0, labels, n_components, stream);
+}
+
+ccl_status ccl_label_threshold(const uint8_t *img, int H, int W, int threshold, int32_t *labels,
+                               int32_t *n_components, ccl_stream_t stream) {
     ccl_status st = check_shape(H, W);
     if (st != CCL_OK) return st;
+    if (threshold < 0 || threshold > 255) return CCL_INVALID_ARGUMENT;
     if ((st = check_buffers(img, labels, n_components, H, W)) != CCL_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Geometry g = make_geometry(H, W);
+    g.thr = threshold;
     size_t offs[32], total;
     workspace_layout(g, offs, &total);
     void *mem = nullptr;
@@ -202,6 +210,12 @@ ccl_status ccl_plan_destroy(ccl_plan p) {
     free_events(p);
     delete p;
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+}
+
+ccl_status ccl_plan_set_threshold(ccl_plan p, int threshold) {
+    if (!p || threshold < 0 || threshold > 255) return CCL_INVALID_ARGUMENT;
+    p->g.thr = threshold;
+    return CCL_OK;
 }
 
 ccl_status ccl_plan_workspace_bytes(ccl_plan p, uint64_t *bytes) {

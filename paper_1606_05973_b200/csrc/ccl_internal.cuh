@@ -36,6 +36,7 @@ struct Geometry {
     int capb;      // border components per tile bound: 2*maxrun + min(H,TH)
     int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
     int row0;      // global row of this image's row 0 (row bands of a sharded image; else 0)
+    int thr;       // foreground <=> byte > thr (0: byte != 0)
 };
 
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).

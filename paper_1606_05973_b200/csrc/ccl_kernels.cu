@@ -244,25 +244,48 @@ __device__ __forceinline__ uint32_t pack16(uint4 v) {
     return pack8(v.x, v.y) | (pack8(v.z, v.w) << 8);
 }
 
+// Threshold on load (the paper's im2bw step,
+// PAPER.md:1084-1089): foreground <=> byte > thr.  Bit 7 of every byte of the
+// result is that flag: the carry out of the low 7 bits of a + ~t decides it
+// (a majority of a7, ~t7 and that carry), no byte borrows from its neighbour.
+__device__ __forceinline__ uint32_t gt_flags(uint32_t a, uint32_t t4) {
+    const uint32_t s = (a & 0x7F7F7F7Fu) + (~t4 & 0x7F7F7F7Fu);
+    return (a & ~t4) | ((a | ~t4) & s);
+}
+__device__ __forceinline__ uint32_t pack8_gt(uint32_t a, uint32_t b, uint32_t t4) {
+    const uint32_t v = ((gt_flags(a, t4) >> 7) & 0x01010101u) | ((gt_flags(b, t4) >> 3) & 0x10101010u);
+    return (v * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t pack16_gt(uint4 v, uint32_t t4) {
+    return pack8_gt(v.x, v.y, t4) | (pack8_gt(v.z, v.w, t4) << 8);
+}
+// 16 bytes -> 16 foreground bits (THR: byte > thr, else byte != 0)
+template <bool THR>
+__device__ __forceinline__ uint32_t pack16_fg(uint4 v, uint32_t thr) {
+    return THR ? pack16_gt(v, thr * 0x01010101u) : pack16(v);
+}
+
 // Rows whose length is not a multiple of 16 bytes: byte loads (kept out of line).
-__device__ __noinline__ uint32_t load_word_bytes(const uint8_t *src, int n) {
+__device__ __noinline__ uint32_t load_word_bytes(const uint8_t *src, int n, uint32_t thr) {
     uint32_t m = 0;
 #pragma unroll 1
-    for (int i = 0; i < n; i++) m |= (uint32_t)(__ldcs(src + i) != 0) << i;
+    for (int i = 0; i < n; i++) m |= (uint32_t)(__ldcs(src + i) > thr) << i;
     return m;
 }
 
 // Load the 32 pixels of lane-word (row, word) as a bitmask.
+template <bool THR>
 __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, const Geometry &g,
                                               int row, int col0) {
     if (col0 >= g.W) return 0u;
     const uint8_t *src = img + (int64_t)row * g.W + col0;
+    const uint32_t thr = THR ? (uint32_t)g.thr : 0u;
     if (g.aligned) {
-        uint32_t m = pack16(__ldcs(reinterpret_cast<const uint4 *>(src)));
-        if (col0 + 16 < g.W) m |= pack16(__ldcs(reinterpret_cast<const uint4 *>(src + 16))) << 16;
+        uint32_t m = pack16_fg<THR>(__ldcs(reinterpret_cast<const uint4 *>(src)), thr);
+        if (col0 + 16 < g.W) m |= pack16_fg<THR>(__ldcs(reinterpret_cast<const uint4 *>(src + 16)), thr) << 16;
         return m;
     }
-    return load_word_bytes(src, min(32, g.W - col0));
+    return load_word_bytes(src, min(32, g.W - col0), thr);
 }
 
 // Run mask of image row `row`, word `gword` (lane = word within the tile
@@ -338,6 +361,9 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
     return ((u << 2) | (up >> 30)) & ((d << 1) | (dp >> 31));
 }
 
+// THR: foreground <=> byte > g.thr (threshold on load) instead of byte != 0;
+// a separate instantiation so the plain path carries no threshold code.
+template <bool THR>
 __global__ void __launch_bounds__(NW * 32, 5)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
     pdl_trigger();
@@ -372,8 +398,9 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         }
     }
     // ---- P0: the pixels of the tile, read once with 16-byte streaming loads:
-    // fg = byte != 0 (reading A10), one bit per pixel.  The
-    // warp's S rows are all in flight before the first is used.
+    // fg = byte != 0 (reading A10) -- or byte > thr when a
+    // threshold is set -- one bit per pixel.  The warp's S rows are all in
+    // flight before the first is used.
     uint32_t xs[S];
     if (g.aligned && C0 + TW <= g.W && rows == TH) {  // interior tile: all 2*S loads in flight
         const uint8_t *src = img + (int64_t)(R0 + r0) * g.W + C0 + 32 * lane;
@@ -383,12 +410,18 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             v[2 * i] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W));
             v[2 * i + 1] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W + 16));
         }
+        if (!THR) {
 #pragma unroll
-        for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+            for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+        } else {
+            const uint32_t t4 = (uint32_t)g.thr * 0x01010101u;
+#pragma unroll
+            for (int i = 0; i < S; i++) xs[i] = pack16_gt(v[2 * i], t4) | (pack16_gt(v[2 * i + 1], t4) << 16);
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < S; i++)
-            xs[i] = (r0 + i < rows && gword < g.WW) ? load_word(img, g, R0 + r0 + i, 32 * gword) : 0u;
+            xs[i] = (r0 + i < rows && gword < g.WW) ? load_word<THR>(img, g, R0 + r0 + i, 32 * gword) : 0u;
     }
     pdl_wait();  // the previous call's kernels are done with the workspace
     if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
@@ -1104,13 +1137,15 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned bl
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tile_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_tile_local<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(K1Smem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_tile_local<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local, NW * 32,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false>, NW * 32,
                                                            sizeof(K1Smem))) != cudaSuccess)
         return e;
     g_k1_resident = sms * per;
@@ -1126,8 +1161,8 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    e = launch_pdl(k_tile_local, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws,
-                   g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
+    e = launch_pdl(g.thr ? k_tile_local<true> : k_tile_local<false>, g.nT, NW * 32, sizeof(K1Smem), stream, img,
+                   g, ws, g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
     if (g_k1_stop < 99) return cudaGetLastError();

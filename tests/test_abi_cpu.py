@@ -66,6 +66,12 @@ def test_argument_validation_without_gpu(lib):
     assert lib.ccl_plan_create(4, 4, None) == 1
     lib.ccl_plan_label.argtypes = [vp, vp, vp, vp, vp]
     assert lib.ccl_plan_label(None, fake, other, n, None) == 1
+    lib.ccl_label_threshold.argtypes = [vp, i, i, i, vp, vp, vp]
+    assert lib.ccl_label_threshold(fake, 4, 4, -1, other, n, None) == 1   # threshold < 0
+    assert lib.ccl_label_threshold(fake, 4, 4, 256, other, n, None) == 1  # threshold > 255
+    assert lib.ccl_label_threshold(fake, 0, 4, 127, other, n, None) == 1
+    lib.ccl_plan_set_threshold.argtypes = [vp, i]
+    assert lib.ccl_plan_set_threshold(None, 127) == 1
     lib.ccl_label_sharded.argtypes = [vp, i, i, i, i, vp, vp, vp, vp]
     assert lib.ccl_label_sharded(fake, 4, 4, 0, 4, other, n, None, None) == 1  # no comm
     assert lib.ccl_label_sharded(fake, 4, 4, 2, 4, other, n, fake, None) == 1  # band past H_total

@@ -137,3 +137,26 @@ def test_rules_random():
         la, _ = pins.bfs_label(img)
         assert same_partition(img, la, pins.bfs_label(fill(img))[0])
         assert same_partition(img, la, model_label(fill(img)))
+
+
+def test_threshold_bit_trick_all_byte_pairs():
+    """K1's threshold-on-load predicate (gt_flags in ccl_kernels.cu): bit 7 of
+    every byte of (a & ~t) | ((a | ~t) & ((a & 0x7F..) + (~t & 0x7F..))) is
+    (a_byte > t_byte), with no interference between the four bytes; checked
+    against the definition for every (byte, threshold) pair in every lane of
+    the word, with random neighbours."""
+    rng = np.random.default_rng(5)
+    a = np.arange(256, dtype=np.uint64)[:, None]
+    t = np.arange(256, dtype=np.uint64)[None, :]
+    M = np.uint64(0xFFFFFFFF)
+    for lane in range(4):
+        noise = rng.integers(0, 256, size=(256, 256, 3)).astype(np.uint64)
+        sh = np.uint64(8 * lane)
+        # the tested byte sits in byte `lane`, the other three are random
+        others = [k for k in range(4) if k != lane]
+        A = (a << sh) + sum(noise[:, :, i] << np.uint64(8 * k) for i, k in enumerate(others))
+        T4 = (t * np.uint64(0x01010101)) & M
+        s = ((A & np.uint64(0x7F7F7F7F)) + (~T4 & np.uint64(0x7F7F7F7F))) & M
+        f = ((A & ~T4) | ((A | ~T4) & s)) & M
+        got = (f >> (sh + np.uint64(7))) & np.uint64(1)
+        assert np.array_equal(got.astype(bool), np.broadcast_to(a > t, got.shape))
