@@ -88,6 +88,20 @@ ccl_status ccl_label_threshold(const uint8_t *img, int H, int W, int threshold, 
                                int32_t *n_components, ccl_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * ccl_label_batch -- B independent images of H x W in one call (SURVEY.md
+ * section 8(f) row f3: the paper's images of 1 MB or less, PAPER.md:1172-1177,
+ * where one image is too small to fill a GPU and launches dominate).
+ *   imgs          DEVICE pointer, B*H*W bytes: image b is rows b*H..b*H+H-1
+ *   labels        DEVICE pointer, B*H*W int32, written; image b's labels are
+ *                 1..N_b in raster order of its own components (as ccl_label)
+ *   n_components  DEVICE pointer to B int32, written: N_b
+ * No component crosses from one image to the next.  B >= 1; (int64)B*H*W
+ * <= INT32_MAX else CCL_TOO_LARGE.  Same ownership/asynchrony as ccl_label.
+ * ---------------------------------------------------------------------- */
+ccl_status ccl_label_batch(const uint8_t *imgs, int B, int H, int W, int32_t *labels,
+                           int32_t *n_components, ccl_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * Plans: preallocate the workspace for one image shape once, then label many
  * images of that shape with no allocation.  A plan may be used by one stream
  * at a time.
@@ -96,6 +110,9 @@ typedef struct ccl_plan_st *ccl_plan;
 
 /* Allocates device workspace for H x W images on the current device. */
 ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out);
+/* Workspace for batches of B images of H x W (ccl_label_batch's layout): the
+ * plan's label calls then take B*H*W pixels and write B component counts. */
+ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out);
 ccl_status ccl_plan_destroy(ccl_plan plan);
 /* Foreground <=> byte > threshold for the plan's later calls (0..255; the
  * default 0 is byte != 0).  See ccl_label_threshold. */

@@ -35,6 +35,10 @@ _L.ccl_label_threshold.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
 _L.ccl_label_threshold.restype = _i
 _L.ccl_plan_set_threshold.argtypes = [_vp, _i]
 _L.ccl_plan_set_threshold.restype = _i
+_L.ccl_label_batch.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
+_L.ccl_label_batch.restype = _i
+_L.ccl_plan_create_batch.argtypes = [_i, _i, _i, ctypes.POINTER(_vp)]
+_L.ccl_plan_create_batch.restype = _i
 _L.ccl_plan_create.argtypes = [_i, _i, ctypes.POINTER(_vp)]
 _L.ccl_plan_create.restype = _i
 _L.ccl_plan_destroy.argtypes = [_vp]
@@ -124,15 +128,40 @@ def label(img, out=None, n_out=None, stream=None, threshold=None):
     return out, n_out
 
 
-class Plan:
-    """Preallocated workspace for one image shape (ccl_plan_* in include/ccl.h)."""
+def label_batch(imgs, out=None, n_out=None, stream=None):
+    """Labels B independent images: a contiguous (B, H, W) uint8 CUDA tensor
+    (ccl_label_batch).  Returns (labels int32 (B, H, W), n_components int32 (B,));
+    every image is numbered 1..N_b on its own."""
+    if not isinstance(imgs, torch.Tensor) or imgs.dtype != torch.uint8 or imgs.dim() != 3:
+        raise TypeError("imgs must be a 3-D torch.uint8 tensor (B, H, W)")
+    if not imgs.is_cuda or not imgs.is_contiguous():
+        raise TypeError("imgs must be a contiguous CUDA tensor")
+    B, H, W = imgs.shape
+    if out is None:
+        out = torch.empty((B, H, W), dtype=torch.int32, device=imgs.device)
+    if n_out is None:
+        n_out = torch.empty(B, dtype=torch.int32, device=imgs.device)
+    _check(_L.ccl_label_batch(imgs.data_ptr(), B, H, W, out.data_ptr(), n_out.data_ptr(),
+                              _stream_handle(stream)), "ccl_label_batch")
+    return out, n_out
 
-    def __init__(self, H, W, device=None):
+
+class Plan:
+    """Preallocated workspace for one image shape (ccl_plan_* in include/ccl.h);
+    batch=B: B images of H x W per call (label() then takes (B, H, W) and
+    returns B counts)."""
+
+    def __init__(self, H, W, device=None, batch=None):
         self.H, self.W = int(H), int(W)
+        self.B = None if batch is None else int(batch)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self._p = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _check(_L.ccl_plan_create(self.H, self.W, ctypes.byref(self._p)), "ccl_plan_create")
+            if self.B is None:
+                _check(_L.ccl_plan_create(self.H, self.W, ctypes.byref(self._p)), "ccl_plan_create")
+            else:
+                _check(_L.ccl_plan_create_batch(self.B, self.H, self.W, ctypes.byref(self._p)),
+                       "ccl_plan_create_batch")
 
     def set_threshold(self, threshold):
         """Foreground <=> byte > threshold for later label() calls (0 = byte != 0)."""
@@ -144,13 +173,16 @@ class Plan:
         return b.value
 
     def label(self, img, out=None, n_out=None, stream=None):
-        _check_img(img)
-        if tuple(img.shape) != (self.H, self.W):
-            raise ValueError(f"plan is for {self.H}x{self.W}, got {tuple(img.shape)}")
+        shape = (self.H, self.W) if self.B is None else (self.B, self.H, self.W)
+        if not isinstance(img, torch.Tensor) or img.dtype != torch.uint8 or not img.is_cuda \
+                or not img.is_contiguous():
+            raise TypeError("img must be a contiguous torch.uint8 CUDA tensor")
+        if tuple(img.shape) != shape:
+            raise ValueError(f"plan is for {shape}, got {tuple(img.shape)}")
         if out is None:
-            out = torch.empty((self.H, self.W), dtype=torch.int32, device=img.device)
+            out = torch.empty(shape, dtype=torch.int32, device=img.device)
         if n_out is None:
-            n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+            n_out = torch.empty(1 if self.B is None else self.B, dtype=torch.int32, device=img.device)
         _check(_L.ccl_plan_label(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
                                  _stream_handle(stream)), "ccl_plan_label")
         return out, n_out

@@ -11,16 +11,21 @@
 
 namespace cclb {
 
-Geometry make_geometry(int H, int W) {
+Geometry make_geometry(int H, int W) { return make_geometry_batch(1, H, W); }
+
+Geometry make_geometry_batch(int B, int IH, int W) {
     Geometry g;
+    const int H = B * IH;
     g.H = H;
     g.W = W;
+    g.IH = IH;
+    g.tpi = (IH + TH - 1) / TH;
     g.WW = (W + 31) / 32;
     g.nTx = (W + TW - 1) / TW;
-    g.nTy = (H + TH - 1) / TH;
+    g.nTy = B * g.tpi;
     g.nT = g.nTx * g.nTy;
     g.nseg = H * g.nTx;
-    const int tw = W < TW ? W : TW, th = H < TH ? H : TH;
+    const int tw = W < TW ? W : TW, th = IH < TH ? IH : TH;
     g.maxrun = (tw + 1) / 2;
     g.capc = ((th + 1) / 2) * g.maxrun;
     g.capb = 2 * g.maxrun + th;
@@ -158,14 +163,29 @@ ccl_status ccl_label(const uint8_t *img, int H, int W, int32_t *labels, int32_t 
     return ccl_label_threshold(img, H, W, 0, labels, n_components, stream);
 }
 
+static ccl_status label_oneshot(const uint8_t *img, int B, int H, int W, int threshold, int32_t *labels,
+                                int32_t *n_components, ccl_stream_t stream);
+
 ccl_status ccl_label_threshold(const uint8_t *img, int H, int W, int threshold, int32_t *labels,
                                int32_t *n_components, ccl_stream_t stream) {
+    return label_oneshot(img, 1, H, W, threshold, labels, n_components, stream);
+}
+
+ccl_status ccl_label_batch(const uint8_t *imgs, int B, int H, int W, int32_t *labels,
+                           int32_t *n_components, ccl_stream_t stream) {
+    return label_oneshot(imgs, B, H, W, 0, labels, n_components, stream);
+}
+
+static ccl_status label_oneshot(const uint8_t *img, int B, int H, int W, int threshold, int32_t *labels,
+                                int32_t *n_components, ccl_stream_t stream) {
+    if (B < 1) return CCL_INVALID_ARGUMENT;
     ccl_status st = check_shape(H, W);
     if (st != CCL_OK) return st;
+    if ((int64_t)B * H > INT32_MAX || (st = check_shape(B * H, W)) != CCL_OK) return CCL_TOO_LARGE;
     if (threshold < 0 || threshold > 255) return CCL_INVALID_ARGUMENT;
-    if ((st = check_buffers(img, labels, n_components, H, W)) != CCL_OK) return st;
+    if ((st = check_buffers(img, labels, n_components, B * H, W)) != CCL_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    Geometry g = make_geometry(H, W);
+    Geometry g = make_geometry_batch(B, H, W);
     g.thr = threshold;
     size_t offs[32], total;
     workspace_layout(g, offs, &total);
@@ -181,13 +201,19 @@ ccl_status ccl_label_threshold(const uint8_t *img, int H, int W, int threshold, 
 }
 
 ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out) {
+    return ccl_plan_create_batch(1, H, W, plan_out);
+}
+
+ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out) {
     if (!plan_out) return CCL_INVALID_ARGUMENT;
     *plan_out = nullptr;
+    if (B < 1) return CCL_INVALID_ARGUMENT;
     ccl_status st = check_shape(H, W);
     if (st != CCL_OK) return st;
+    if ((int64_t)B * H > INT32_MAX || check_shape(B * H, W) != CCL_OK) return CCL_TOO_LARGE;
     ccl_plan p = new (std::nothrow) ccl_plan_st;
     if (!p) return CCL_OUT_OF_MEMORY;
-    p->g = make_geometry(H, W);
+    p->g = make_geometry_batch(B, H, W);
     size_t offs[32];
     workspace_layout(p->g, offs, &p->ws_bytes);
     cudaError_t e = cudaMalloc(&p->ws_mem, p->ws_bytes);
@@ -248,7 +274,7 @@ ccl_status ccl_plan_label_host(ccl_plan p, const uint8_t *h_img, int32_t *h_labe
     if (!p->d_img) {
         if ((e = cudaMalloc(&p->d_img, n)) != cudaSuccess ||
             (e = cudaMalloc(&p->d_lab, n * 4)) != cudaSuccess ||
-            (e = cudaMalloc(&p->d_n, 16)) != cudaSuccess)
+            (e = cudaMalloc(&p->d_n, sizeof(int32_t) * (p->g.nTy / p->g.tpi))) != cudaSuccess)
             return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
     }
     if (cudaMemcpyAsync(p->d_img, h_img, n, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -256,7 +282,8 @@ ccl_status ccl_plan_label_host(ccl_plan p, const uint8_t *h_img, int32_t *h_labe
     ccl_status st = ccl_plan_label(p, p->d_img, p->d_lab, p->d_n, stream);
     if (st != CCL_OK) return st;
     if (cudaMemcpyAsync(h_labels, p->d_lab, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(h_n_components, p->d_n, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        cudaMemcpyAsync(h_n_components, p->d_n, sizeof(int32_t) * (p->g.nTy / p->g.tpi), cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess)
         return CCL_CUDA_ERROR;
     return cudaStreamSynchronize(s) == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
 }

@@ -35,6 +35,8 @@ struct Geometry {
     int capc;      // components per tile bound: ceil(min(H,TH)/2) * maxrun
     int capb;      // border components per tile bound: 2*maxrun + min(H,TH)
     int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
+    int IH;        // rows per image: a batch is B images of IH x W stacked in memory (H = B*IH)
+    int tpi;       // tile rows per image = ceil(IH/TH); tile rows never straddle two images
     int row0;      // global row of this image's row 0 (row bands of a sharded image; else 0)
     int thr;       // foreground <=> byte > thr (0: byte != 0)
 };
@@ -66,6 +68,23 @@ struct Workspace {
 };
 
 Geometry make_geometry(int H, int W);
+// B images of IH x W, contiguous (image b = rows b*IH .. b*IH+IH-1 of a B*IH x W image)
+Geometry make_geometry_batch(int B, int IH, int W);
+
+// Tile row ty: first memory row, rows; tile row of a memory row.
+// (a single image -- tpi == nTy -- takes the division-free branch)
+__host__ __device__ __forceinline__ int tile_r0(const Geometry &g, int ty) {
+    if (g.tpi == g.nTy) return ty * TH;
+    return (ty / g.tpi) * g.IH + (ty % g.tpi) * TH;
+}
+__host__ __device__ __forceinline__ int tile_rows(const Geometry &g, int ty) {
+    const int r = g.tpi == g.nTy ? g.H - ty * TH : g.IH - (ty % g.tpi) * TH;
+    return r < TH ? r : TH;
+}
+__host__ __device__ __forceinline__ int row_tile(const Geometry &g, int row) {
+    if (g.tpi == g.nTy) return row / TH;
+    return (row / g.IH) * g.tpi + (row % g.IH) / TH;
+}
 // Offsets of every Workspace array inside one allocation of *total bytes.
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);

@@ -296,7 +296,7 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
 __device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *__restrict__ bm,
                                              int row, int gword, uint32_t *fg) {
     const int lane = lane_id();
-    const int R0 = (row / TH) * TH, rl = row - R0, rows = min(TH, g.H - R0);
+    const int ty = row_tile(g, row), R0 = tile_r0(g, ty), rl = row - R0, rows = tile_rows(g, ty);
     const bool ok = gword < g.WW;
     const int64_t i = (int64_t)row * g.WW + gword;
     const uint32_t x0 = ok ? __ldcg(bm + i) : 0u;
@@ -363,7 +363,9 @@ __device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32
 
 // THR: foreground <=> byte > g.thr (threshold on load) instead of byte != 0;
 // a separate instantiation so the plain path carries no threshold code.
-template <bool THR>
+// BATCH: a stack of images (tile rows are placed per image); the single-image
+// instantiation keeps the plain row arithmetic.
+template <bool THR, bool BATCH>
 __global__ void __launch_bounds__(NW * 32, 5)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
     pdl_trigger();
@@ -373,8 +375,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int tx = blockIdx.x % g.nTx, ty = blockIdx.x / g.nTx;
     const int tile = blockIdx.x;
-    const int R0 = ty * TH, C0 = tx * TW;
-    const int rows = min(TH, g.H - R0);
+    const int R0 = BATCH ? tile_r0(g, ty) : ty * TH, C0 = tx * TW;
+    const int rows = BATCH ? tile_rows(g, ty) : min(TH, g.H - R0);
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;  // this lane's word index in the image row
     const int r0 = w * S;
@@ -387,9 +389,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     {
         const int pt = blockIdx.x + pfd;
         if (pfd > 0 && pt < g.nT) {
-            const int prow = (pt / g.nTx) * TH + (threadIdx.x >> 3);
+            const int pty = pt / g.nTx;
+            const int prow = (BATCH ? tile_r0(g, pty) : pty * TH) + (threadIdx.x >> 3);
             const int pcol = (pt % g.nTx) * TW + (threadIdx.x & 7) * 128;
-            if (prow < g.H && pcol < g.W) {
+            if ((BATCH ? (int)(threadIdx.x >> 3) < tile_rows(g, pty) : prow < g.H) && pcol < g.W) {
                 const uint8_t *a = img + (int64_t)prow * g.W + pcol;
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
                 if ((threadIdx.x & 7) == 7 && pcol + 127 < g.W)
@@ -691,7 +694,8 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     const int gw = blockIdx.x * 8 + wib;
     if (gw < nh_warps) {
         const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
-        const int ru = ty * TH - 1, rx = ty * TH;
+        if (ty % g.tpi == 0) return;  // first tile row of an image of a batch: no edge
+        const int rx = tile_r0(g, ty), ru = rx - 1;
         const int gword = tx * WPR + lane;
         const uint32_t u = run_mask(g, ws.bm, ru, gword, nullptr);
         const uint32_t x = run_mask(g, ws.bm, rx, gword, nullptr);
@@ -748,8 +752,10 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     }
     const int ap = __shfl_up_sync(FULL, a, 1), bp = __shfl_up_sync(FULL, b, 1);
     const int an = __shfl_down_sync(FULL, a, 1), bn = __shfl_down_sync(FULL, b, 1);
-    const bool up_ok = lane > 0 && r > 0;         // lane-1 is row r-1 of this edge
-    const bool dn_ok = lane < 31 && r + 1 < g.H;  // lane+1 is row r+1 of this edge
+    // rows r-1 / r+1 of the same image (a batch stacks images: no edges across)
+    const bool has_up = r % g.IH != 0, has_dn = r + 1 < g.H && (r + 1) % g.IH != 0;
+    const bool up_ok = lane > 0 && has_up;   // lane-1 is row r-1 of this edge
+    const bool dn_ok = lane < 31 && has_dn;  // lane+1 is row r+1 of this edge
     if (a < 0) return;
     if (b >= 0) {
         // (r-1) and (r+1) are then joined through b
@@ -757,11 +763,11 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         return;
     }
     // diagonal neighbours; skipped when the adjacent row makes the same union
-    if (r > 0) {
+    if (has_up) {
         const int bu = L[r - 1];
         if (bu >= 0 && !(up_ok && ap == a && bp == bu)) gunion(ws.gparent, ws.gkey, a, bu);
     }
-    if (r + 1 < g.H) {
+    if (has_dn) {
         const int bd = L[r + 1];
         if (bd >= 0 && !(dn_ok && an == a && bn == bd)) gunion(ws.gparent, ws.gkey, a, bd);
     }
@@ -813,7 +819,8 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
     __syncthreads();
     const int ty = sm.part;
-    const int R0 = ty * TH, rows = min(TH, g.H - R0);
+    const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
+    const bool first = ty % g.tpi == 0;  // first tile row of its image: numbering starts at 1
     // ---- phase 1: root counts of the segments (R0 + r, tx)
     for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
         const int tile = ty * g.nTx + tx;
@@ -861,9 +868,9 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     // bits value.  Warp 0 looks back over 32 predecessors at a time.
     if (w == 0) {
         if (lane == 0)
-            atomicExch(ws.scanstate + ty, ((ty == 0 ? 2ull : 1ull) << 62) | (uint32_t)carry);
+            atomicExch(ws.scanstate + ty, ((first ? 2ull : 1ull) << 62) | (uint32_t)carry);
         int excl = 0;
-        if (ty > 0) {
+        if (!first) {
             const volatile unsigned long long *st = ws.scanstate;
             int j = ty - 1;
             while (true) {
@@ -888,7 +895,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         }
         if (lane == 0) {
             sm.excl = excl;
-            if (ty == g.nTy - 1) *n_components = excl + carry;
+            if (ty % g.tpi == g.tpi - 1) n_components[ty / g.tpi] = excl + carry;
         }
     }
     __syncthreads();
@@ -917,7 +924,7 @@ k_label(Geometry g, Workspace ws) {
     const int tile = blockIdx.x * KL_WARPS + w;
     if (tile >= g.nT) return;
     const int tx = tile % g.nTx, ty = tile / g.nTx;
-    const int R0 = ty * TH, rows = min(TH, g.H - R0);
+    const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
     const int32_t *meta = ws.meta + (int64_t)tile * META;
     const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
     const int f = __ldcg(meta + META_ROWFIRST + lane);
@@ -1011,7 +1018,7 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
     const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
     if (seg >= g.nseg) return;
     const int row = (int)(seg / g.nTx), tx = (int)(seg % g.nTx);
-    const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
+    const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
     const uint16_t *rc = ws.runcomp + seg * g.maxrun;
@@ -1070,7 +1077,7 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     const int lane = lane_id();
     const int tx = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (tx >= g.nTx) return;
-    const int C0 = tx * TW, tile = (row / TH) * g.nTx + tx;
+    const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
     const int gword = tx * WPR + lane;
     uint32_t x;
     const uint32_t f = run_mask(g, ws.bm, row, gword, &x);
@@ -1137,15 +1144,16 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned bl
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_tile_local<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(K1Smem));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_tile_local<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem));
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    for (auto k : {k_tile_local<false, false>, k_tile_local<true, false>, k_tile_local<false, true>,
+                   k_tile_local<true, true>})
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))) !=
+            cudaSuccess)
+            return e;
     int dev = 0, sms = 0, per = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false>, NW * 32,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false, false>, NW * 32,
                                                            sizeof(K1Smem))) != cudaSuccess)
         return e;
     g_k1_resident = sms * per;
@@ -1161,8 +1169,11 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    e = launch_pdl(g.thr ? k_tile_local<true> : k_tile_local<false>, g.nT, NW * 32, sizeof(K1Smem), stream, img,
-                   g, ws, g_k1_exper ? 0 : g_k1_resident, g_k1_stop);
+    const bool batch = g.tpi != g.nTy;
+    auto k1 = g.thr ? (batch ? k_tile_local<true, true> : k_tile_local<true, false>)
+                    : (batch ? k_tile_local<false, true> : k_tile_local<false, false>);
+    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_exper ? 0 : g_k1_resident,
+                   g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
     if (g_k1_stop < 99) return cudaGetLastError();

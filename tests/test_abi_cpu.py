@@ -70,6 +70,13 @@ def test_argument_validation_without_gpu(lib):
     assert lib.ccl_label_threshold(fake, 4, 4, -1, other, n, None) == 1   # threshold < 0
     assert lib.ccl_label_threshold(fake, 4, 4, 256, other, n, None) == 1  # threshold > 255
     assert lib.ccl_label_threshold(fake, 0, 4, 127, other, n, None) == 1
+    lib.ccl_label_batch.argtypes = [vp, i, i, i, vp, vp, vp]
+    assert lib.ccl_label_batch(fake, 0, 4, 4, other, n, None) == 1      # B < 1
+    assert lib.ccl_label_batch(fake, 2, 0, 4, other, n, None) == 1      # H < 1
+    assert lib.ccl_label_batch(fake, 70000, 200, 200, other, n, None) == 2  # B*H*W > INT32_MAX
+    lib.ccl_plan_create_batch.argtypes = [i, i, i, ctypes.POINTER(vp)]
+    assert lib.ccl_plan_create_batch(0, 4, 4, ctypes.byref(p)) == 1
+    assert lib.ccl_plan_create_batch(70000, 200, 200, ctypes.byref(p)) == 2
     lib.ccl_plan_set_threshold.argtypes = [vp, i]
     assert lib.ccl_plan_set_threshold(None, 127) == 1
     lib.ccl_label_sharded.argtypes = [vp, i, i, i, i, vp, vp, vp, vp]
