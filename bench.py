@@ -44,6 +44,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 single vs batched lines")
     return ap.parse_args()
 
 
@@ -133,6 +134,38 @@ def time_oracle(img, runs):
         out = oracle.label(img)
         ts.append(time.perf_counter() - t0)
     return statistics.median(ts), out
+
+
+def small_images(dev, stream, batch=64, reps=20):
+    import numpy as np
+    import torch
+    import synth
+    import paper_1606_05973_b200 as ccl
+    res = {}
+    for name in ["c1_bernoulli_512", "c2_blobs_1024"]:
+        img = synth.generate(name)
+        H, W = img.shape
+        single = torch.from_numpy(img).to(dev)
+        stack = torch.from_numpy(np.stack([img] * batch)).to(dev)
+        p1, pb = ccl.Plan(H, W, device=dev), ccl.Plan(H, W, device=dev, batch=batch)
+        o1, ob = torch.empty((H, W), dtype=torch.int32, device=dev), torch.empty((batch, H, W), dtype=torch.int32, device=dev)
+        n1, nb = torch.empty(1, dtype=torch.int32, device=dev), torch.empty(batch, dtype=torch.int32, device=dev)
+        out = {}
+        for tag, fn, px in (("single", lambda: p1.label(single, o1, n1), H * W),
+                            (f"batch{batch}", lambda: pb.label(stack, ob, nb), batch * H * W)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = a.elapsed_time(b) / reps
+            out[tag] = {"us_per_call": ms * 1e3, "gpx_s": px / (ms * 1e-3) / 1e9}
+        res[name] = out
+    return res
 
 
 def dist_env():
@@ -298,6 +331,11 @@ def main():
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
         "roofline": roofline,
     }
+
+    # ---- the paper's <= 1 MB regime (C1, C2): one image per call vs a batch
+    # of 64 per call (ccl_label_batch), device-resident, CUDA events
+    if ws == 1 and not args.no_small:
+        line["small_images"] = small_images(dev, stream)
 
     # ---- end to end through the public API with host buffers (N=1)
     if ws == 1 and not args.no_e2e:
