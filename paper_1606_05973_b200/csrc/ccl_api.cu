@@ -96,6 +96,7 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.comprow = reinterpret_cast<uint8_t *>(b + offs[A_COMPROW]);
     w.rowexcl = reinterpret_cast<int32_t *>(b + offs[A_ROWEXCL]);
     w.xlab = nullptr;
+    w.boff = nullptr;
     return w;
 }
 

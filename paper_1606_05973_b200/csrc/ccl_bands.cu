@@ -2,24 +2,28 @@
 // analogue of PARemSP's row chunks: every band is labelled
 // locally with keys that carry its global row offset (PARemSP's per-thread
 // label base, "count <- start x col"); the boundary rows of
-// all bands are all-gathered and the small cross-band equivalence graph is
-// resolved (PARemSP's boundary merge); per-band root counts
-// are all-gathered so each band numbers its labels after the earlier bands.
+// all bands are all-gathered and every rank resolves the small cross-band
+// equivalence graph on its GPU (PARemSP's boundary merge);
+// per-band root counts are all-gathered so each band numbers its labels after
+// the earlier bands.  Everything stays on the device and on the stream: no
+// host synchronization inside a call.
 //
 // Protocol per band (the same code drives NCCL ranks and the single-GPU
 // "virtual bands" mode, which only differs in how the three all-gathers move
 // bytes):
-//   A  pack + tile labeling + tile-edge merge of the band (device)
-//      per-pixel root keys of the band's first and last row (device)
-//   X1 all-gather of those keys
-//   B  host: resolve the cross-band classes; a band root whose class minimum
-//      is another key is re-linked -- to that root's node when it is in the
-//      same band, else to a foreign-label slot (-2-f)
+//   A  tile labeling + tile-edge merge of the band; per pixel of its first and
+//      last row the band-local root key and node (2W "slots"), and for every
+//      slot the first slot of the same band-local component
+//   X1 all-gather of slot keys and representatives
+//   B  every rank: union-find over all nb*2W slots (band-local components,
+//      8-adjacency across every band boundary; the smaller key wins), then
+//      this band's components whose class starts elsewhere are linked: to the
+//      other component's node in this band, or to a foreign slot (-2-slot)
 //   C  roots + numbering scan of the band -> N_band
 //   X2 all-gather of N_band -> offset of this band = sum over earlier bands
-//   D  labels of the band's boundary-row roots (device)
-//   X3 all-gather of those labels; host fills the foreign-label table
-//   E  component labels + label write (device)
+//   D  labels of the band's boundary-slot roots
+//   X3 all-gather of those labels = the foreign-label table (slot indexed)
+//   E  labels of merged components + label write
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -93,37 +97,45 @@ struct Band {
     Geometry g;
     Workspace ws;
     void *mem = nullptr;
-    // device buffers: [0] first row, [1] last row
-    int64_t *d_keys = nullptr;  // 2 * W
-    int32_t *d_nodes = nullptr; // 2 * W
-    int32_t *d_exp = nullptr;   // 2 * W
-    int32_t *d_small = nullptr; // [0] N_band
-    int32_t *d_xlab = nullptr;  // foreign labels
-    int2 *d_act = nullptr;      // re-links
-    size_t xlab_cap = 0, act_cap = 0;
-    // host copies
-    std::vector<int64_t> keys;   // 2 * W
-    std::vector<int32_t> nodes;  // 2 * W
-    std::vector<int64_t> fkeys;  // foreign class minima (index f -> key)
+    int32_t *d_nodes = nullptr;    // 2W band-local root node of each slot (-1 background)
+    int32_t *d_noderep = nullptr;  // scratch: first slot of each node
+    size_t noderep_count = 0;
+    int32_t *d_small = nullptr;    // [0] N_band, [1] band offset
     int band_H = 0, row0 = 0;
-    int32_t offset = 0;          // labels of earlier bands (phase D)
 
     ~Band() { release(); }
     void release() {
         if (mem) cudaFree(mem);
-        if (d_keys) cudaFree(d_keys);
         if (d_nodes) cudaFree(d_nodes);
-        if (d_exp) cudaFree(d_exp);
+        if (d_noderep) cudaFree(d_noderep);
         if (d_small) cudaFree(d_small);
-        if (d_xlab) cudaFree(d_xlab);
-        if (d_act) cudaFree(d_act);
         mem = nullptr;
-        d_keys = nullptr;
         d_nodes = nullptr;
-        d_exp = nullptr;
+        d_noderep = nullptr;
         d_small = nullptr;
-        d_xlab = nullptr;
-        d_act = nullptr;
+    }
+};
+
+// Cross-band tables shared by the bands of one image (replicated per rank).
+struct XBand {
+    int nb = 0, W = 0;
+    int64_t *keys = nullptr;  // nb*2W slot keys (-1 background)
+    int32_t *reps = nullptr;  // nb*2W representative slot (band-local index)
+    int32_t *spar = nullptr;  // nb*2W slot union-find
+    int32_t *exps = nullptr;  // nb*2W exported labels
+    int32_t *counts = nullptr;  // nb   N of every band
+    ~XBand() { release(); }
+    void release() {
+        if (keys) cudaFree(keys);
+        if (reps) cudaFree(reps);
+        if (spar) cudaFree(spar);
+        if (exps) cudaFree(exps);
+        if (counts) cudaFree(counts);
+        keys = nullptr;
+        reps = nullptr;
+        spar = nullptr;
+        exps = nullptr;
+        counts = nullptr;
     }
 };
 
@@ -147,117 +159,56 @@ ccl_status band_init(Band &b, int band_H, int W, int row0) {
     workspace_layout(b.g, offs, &total);
     CK(cudaMalloc(&b.mem, total));
     b.ws = workspace_bind(b.g, b.mem);
-    CK(cudaMalloc(&b.d_keys, sizeof(int64_t) * 2 * W));
     CK(cudaMalloc(&b.d_nodes, sizeof(int32_t) * 2 * W));
-    CK(cudaMalloc(&b.d_exp, sizeof(int32_t) * 2 * W));
+    b.noderep_count = (size_t)b.g.nT * b.g.capb;
+    CK(cudaMalloc(&b.d_noderep, sizeof(int32_t) * b.noderep_count));
     CK(cudaMalloc(&b.d_small, sizeof(int32_t) * 4));
-    b.keys.resize(2 * (size_t)W);
-    b.nodes.resize(2 * (size_t)W);
+    b.ws.boff = b.d_small + 1;
     return CCL_OK;
 }
 
-// A: local labeling + boundary-row root keys (device), then copy the keys and
-// nodes to the host.
-ccl_status band_phase_a(Band &b, const uint8_t *img, cudaStream_t s) {
+ccl_status xband_init(XBand &x, int nb, int W) {
+    x.nb = nb;
+    x.W = W;
+    const size_t n = (size_t)nb * 2 * W;
+    CK(cudaMalloc(&x.keys, sizeof(int64_t) * n));
+    CK(cudaMalloc(&x.reps, sizeof(int32_t) * n));
+    CK(cudaMalloc(&x.spar, sizeof(int32_t) * n));
+    CK(cudaMalloc(&x.exps, sizeof(int32_t) * n));
+    CK(cudaMalloc(&x.counts, sizeof(int32_t) * nb));
+    return CCL_OK;
+}
+
+// A: local labeling; slot keys / nodes / representatives into (keys, reps)
+ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, cudaStream_t s) {
     const int W = b.g.W;
     CK(run_stage_local(b.g, b.ws, img, s, nullptr));
-    CK(band_row_roots(b.g, b.ws, 0, b.d_keys, b.d_nodes, s));
-    CK(band_row_roots(b.g, b.ws, b.band_H - 1, b.d_keys + W, b.d_nodes + W, s));
-    CK(cudaMemcpyAsync(b.nodes.data(), b.d_nodes, sizeof(int32_t) * 2 * W, cudaMemcpyDeviceToHost, s));
+    CK(band_row_roots(b.g, b.ws, 0, keys, b.d_nodes, s));
+    CK(band_row_roots(b.g, b.ws, b.band_H - 1, keys + W, b.d_nodes + W, s));
+    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, b.noderep_count, reps, s));
     return CCL_OK;
 }
 
-// B: re-link the band's roots whose cross-band class minimum is another key.
-ccl_status band_phase_b(Band &b, Resolver &res, const std::vector<int> &row0s,
-                        const std::vector<int> &bandHs, int self, cudaStream_t s) {
-    const int W = b.g.W;
-    const int64_t keys_per_row = (int64_t)b.g.nTx * MAXRUN;  // key = grow * keys_per_row + ...
-    std::unordered_map<int64_t, int32_t> own_node;           // key -> node, this band
-    for (int i = 0; i < 2 * W; i++)
-        if (b.keys[i] >= 0) own_node[b.keys[i]] = b.nodes[i];
-    std::unordered_map<int64_t, int32_t> fidx;
-    std::unordered_map<int32_t, int32_t> act;  // node -> new parent
-    b.fkeys.clear();
-    for (const auto &kv : own_node) {
-        const int64_t m = res.class_min(kv.first);
-        if (m == kv.first) continue;
-        const int grow = (int)(m / keys_per_row);
-        int target;
-        if (grow >= b.row0 && grow < b.row0 + b.band_H) {
-            target = own_node.at(m);
-        } else {
-            auto it = fidx.find(m);
-            int f;
-            if (it == fidx.end()) {
-                f = (int)b.fkeys.size();
-                fidx[m] = f;
-                b.fkeys.push_back(m);
-            } else {
-                f = it->second;
-            }
-            target = -2 - f;
-        }
-        act[kv.second] = target;
-    }
-    (void)row0s;
-    (void)bandHs;
-    (void)self;
-    std::vector<int2> h(act.size());
-    size_t i = 0;
-    for (const auto &kv : act) h[i++] = make_int2(kv.first, kv.second);
-    if (h.size() > b.act_cap) {
-        if (b.d_act) cudaFree(b.d_act);
-        b.act_cap = h.size();
-        CK(cudaMalloc(&b.d_act, sizeof(int2) * b.act_cap));
-    }
-    if (!h.empty()) {
-        CK(cudaMemcpyAsync(b.d_act, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice, s));
-        CK(band_apply(b.ws, b.d_act, (int)h.size(), s));
-        CK(cudaStreamSynchronize(s));  // h is a host temporary
-    }
+// B (after the slot tables are complete): link this band's components whose
+// class starts elsewhere.  C: roots + numbering scan -> N_band in counts[self].
+ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s) {
+    CK(band_link(b.ws, x.W, self, x.keys, x.spar, b.d_nodes, s));
+    CK(run_stage_count(b.g, b.ws, count_out, s, nullptr));
     return CCL_OK;
 }
 
-// C: roots + numbering scan of the band; N_band -> d_small[0]
-ccl_status band_phase_c(Band &b, cudaStream_t s) {
-    CK(run_stage_count(b.g, b.ws, b.d_small, s, nullptr));
+// D: with all counts known, the band offset and the labels of its slots' roots
+ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int32_t *exp_out,
+                        cudaStream_t s) {
+    CK(band_offsets(x.nb, self, x.counts, b.d_small + 1, n_total, s));
+    CK(band_export(b.g, b.ws, b.d_nodes, exp_out, 2 * x.W, s));
     return CCL_OK;
 }
 
-// D: with the band offset, the labels of the boundary-row roots
-ccl_status band_phase_d(Band &b, int32_t offset, cudaStream_t s) {
-    const int W = b.g.W;
-    b.offset = offset;
-    CK(band_export(b.g, b.ws, b.d_nodes, b.d_exp, offset, s));
-    CK(band_export(b.g, b.ws, b.d_nodes + W, b.d_exp + W, offset, s));
-    return CCL_OK;
-}
-
-// E: foreign labels from the gathered exports, then the final stage
-ccl_status band_phase_e(Band &b, const int64_t *const *all_keys, const int32_t *const *all_exp,
-                        int nb, int32_t *labels, cudaStream_t s) {
-    const int W = b.g.W;
-    std::vector<int32_t> xl(b.fkeys.size(), 0);
-    if (!b.fkeys.empty()) {
-        std::unordered_map<int64_t, int32_t> lab;
-        for (int j = 0; j < nb; j++)
-            for (int i = 0; i < 2 * W; i++)
-                if (all_exp[j][i] >= 0) lab[all_keys[j][i]] = all_exp[j][i];
-        for (size_t f = 0; f < b.fkeys.size(); f++) {
-            auto it = lab.find(b.fkeys[f]);
-            if (it == lab.end()) return CCL_CUDA_ERROR;  // protocol invariant broken
-            xl[f] = it->second;
-        }
-        if (xl.size() > b.xlab_cap) {
-            if (b.d_xlab) cudaFree(b.d_xlab);
-            b.xlab_cap = xl.size();
-            CK(cudaMalloc(&b.d_xlab, sizeof(int32_t) * b.xlab_cap));
-        }
-        CK(cudaMemcpyAsync(b.d_xlab, xl.data(), sizeof(int32_t) * xl.size(), cudaMemcpyHostToDevice, s));
-    }
-    b.ws.xlab = b.d_xlab;
-    CK(run_stage_final(b.g, b.ws, labels, b.offset, s, nullptr));
-    CK(cudaStreamSynchronize(s));  // xl is a host temporary
+// E: labels of merged components (foreign ones from the exported table) + write
+ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s) {
+    b.ws.xlab = x.exps;
+    CK(run_stage_final(b.g, b.ws, labels, s, nullptr));
     return CCL_OK;
 }
 
@@ -290,58 +241,29 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
         acc += bh[k];
     }
     std::vector<Band> bands(nbands);
-    for (int k = 0; k < nbands; k++) {
-        ccl_status st = band_init(bands[k], bh[k], W, r0[k]);
-        if (st != CCL_OK) return st;
-    }
-    // A + X1
-    std::vector<const int64_t *> rows(2 * nbands);
-    for (int k = 0; k < nbands; k++) {
-        ccl_status st = band_phase_a(bands[k], img + (size_t)r0[k] * W, s);
-        if (st != CCL_OK) return st;
-        CK(cudaMemcpyAsync(bands[k].keys.data(), bands[k].d_keys, sizeof(int64_t) * 2 * W,
-                           cudaMemcpyDeviceToHost, s));
-    }
-    CK(cudaStreamSynchronize(s));
-    for (int k = 0; k < nbands; k++) {
-        rows[2 * k] = bands[k].keys.data();
-        rows[2 * k + 1] = bands[k].keys.data() + W;
-    }
-    Resolver res;
-    res.build(nbands, W, rows.data());
-    // B + C + X2
-    std::vector<int32_t> nband(nbands);
-    for (int k = 0; k < nbands; k++) {
-        ccl_status st = band_phase_b(bands[k], res, r0, bh, k, s);
-        if (st == CCL_OK) st = band_phase_c(bands[k], s);
-        if (st != CCL_OK) return st;
-        CK(cudaMemcpyAsync(&nband[k], bands[k].d_small, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    }
-    CK(cudaStreamSynchronize(s));
-    // D + X3
-    std::vector<std::vector<int32_t>> exps(nbands, std::vector<int32_t>(2 * (size_t)W));
-    int32_t off = 0;
-    for (int k = 0; k < nbands; k++) {
-        ccl_status st = band_phase_d(bands[k], off, s);
-        if (st != CCL_OK) return st;
-        off += nband[k];
-        CK(cudaMemcpyAsync(exps[k].data(), bands[k].d_exp, sizeof(int32_t) * 2 * W, cudaMemcpyDeviceToHost, s));
-    }
-    CK(cudaStreamSynchronize(s));
-    std::vector<const int64_t *> akeys(nbands);
-    std::vector<const int32_t *> aexp(nbands);
-    for (int k = 0; k < nbands; k++) {
-        akeys[k] = bands[k].keys.data();
-        aexp[k] = exps[k].data();
-    }
+    XBand x;
+    ccl_status st = xband_init(x, nbands, W);
+    if (st != CCL_OK) return st;
+    for (int k = 0; k < nbands; k++)
+        if ((st = band_init(bands[k], bh[k], W, r0[k])) != CCL_OK) return st;
+    const size_t slots = 2 * (size_t)W;
+    // A (+ X1: every band writes its slots straight into the shared tables)
+    for (int k = 0; k < nbands; k++)
+        if ((st = band_phase_a(bands[k], img + (size_t)r0[k] * W, x.keys + k * slots, x.reps + k * slots, s)) !=
+            CCL_OK)
+            return st;
+    CK(band_resolve(nbands, W, x.keys, x.reps, x.spar, s));
+    // B + C (+ X2)
+    for (int k = 0; k < nbands; k++)
+        if ((st = band_phase_bc(bands[k], x, k, x.counts + k, s)) != CCL_OK) return st;
+    // D (+ X3)
+    for (int k = 0; k < nbands; k++)
+        if ((st = band_phase_d(bands[k], x, k, k == 0 ? n_components : nullptr, x.exps + k * slots, s)) != CCL_OK)
+            return st;
     // E
-    for (int k = 0; k < nbands; k++) {
-        ccl_status st = band_phase_e(bands[k], akeys.data(), aexp.data(), nbands,
-                                     labels + (size_t)r0[k] * W, s);
-        if (st != CCL_OK) return st;
-    }
-    CK(cudaMemcpyAsync(n_components, &off, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < nbands; k++)
+        if ((st = band_phase_e(bands[k], x, labels + (size_t)r0[k] * W, s)) != CCL_OK) return st;
+    CK(cudaStreamSynchronize(s));  // the band workspaces are freed on return
     return CCL_OK;
 }
 
@@ -349,18 +271,9 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
 
 struct ccl_shard_plan_st {
     Band b;
+    XBand x;
     ncclComm_t comm = nullptr;
     int nranks = 0, rank = 0, W = 0;
-    int32_t total = 0;
-    int64_t *d_allkeys = nullptr;
-    int32_t *d_allexp = nullptr, *d_alln = nullptr;
-    std::vector<int64_t> allkeys;
-    std::vector<int32_t> allexp, nband;
-    ~ccl_shard_plan_st() {
-        if (d_allkeys) cudaFree(d_allkeys);
-        if (d_allexp) cudaFree(d_allexp);
-        if (d_alln) cudaFree(d_alln);
-    }
 };
 
 extern "C" {
@@ -402,19 +315,11 @@ ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_n
     p->rank = rank;
     p->W = W;
     ccl_status st = band_init(p->b, band_H, W, row0);
+    if (st == CCL_OK) st = xband_init(p->x, nranks, W);
     if (st != CCL_OK) {
         delete p;
         return st;
     }
-    if (cudaMalloc(&p->d_allkeys, sizeof(int64_t) * 2 * W * nranks) != cudaSuccess ||
-        cudaMalloc(&p->d_allexp, sizeof(int32_t) * 2 * W * nranks) != cudaSuccess ||
-        cudaMalloc(&p->d_alln, sizeof(int32_t) * nranks) != cudaSuccess) {
-        delete p;
-        return CCL_OUT_OF_MEMORY;
-    }
-    p->allkeys.resize(2 * (size_t)W * nranks);
-    p->allexp.resize(2 * (size_t)W * nranks);
-    p->nband.resize(nranks);
     *plan_out = p;
     return CCL_OK;
 }
@@ -430,54 +335,25 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     if (!p || !band_img || !band_labels || !n_components) return CCL_INVALID_ARGUMENT;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     Band &b = p->b;
-    const int W = p->W, nranks = p->nranks, rank = p->rank;
-    // A + X1
-    ccl_status st = band_phase_a(b, band_img, s);
+    XBand &x = p->x;
+    const size_t slots = 2 * (size_t)p->W;
+    const int self = p->rank;
+    // A + X1 (own slots written in place, then gathered)
+    ccl_status st = band_phase_a(b, band_img, x.keys + self * slots, x.reps + self * slots, s);
     if (st != CCL_OK) return st;
-    CKN(ncclAllGather(b.d_keys, p->d_allkeys, 2 * (size_t)W, ncclInt64, p->comm, s));
-    CK(cudaMemcpyAsync(p->allkeys.data(), p->d_allkeys, sizeof(int64_t) * p->allkeys.size(),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    memcpy(b.keys.data(), p->allkeys.data() + 2 * (size_t)W * rank, sizeof(int64_t) * 2 * W);
-    std::vector<const int64_t *> rows(2 * nranks);
-    for (int k = 0; k < nranks; k++) {
-        rows[2 * k] = p->allkeys.data() + 2 * (size_t)W * k;
-        rows[2 * k + 1] = rows[2 * k] + W;
-    }
-    Resolver res;
-    res.build(nranks, W, rows.data());
+    CKN(ncclGroupStart());
+    CKN(ncclAllGather(x.keys + self * slots, x.keys, slots, ncclInt64, p->comm, s));
+    CKN(ncclAllGather(x.reps + self * slots, x.reps, slots, ncclInt32, p->comm, s));
+    CKN(ncclGroupEnd());
     // B + C + X2
-    st = band_phase_b(b, res, {}, {}, rank, s);
-    if (st == CCL_OK) st = band_phase_c(b, s);
-    if (st != CCL_OK) return st;
-    CKN(ncclAllGather(b.d_small, p->d_alln, 1, ncclInt32, p->comm, s));
-    CK(cudaMemcpyAsync(p->nband.data(), p->d_alln, sizeof(int32_t) * nranks, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    int32_t off = 0, total = 0;
-    for (int k = 0; k < nranks; k++) {
-        if (k < rank) off += p->nband[k];
-        total += p->nband[k];
-    }
+    CK(band_resolve(p->nranks, p->W, x.keys, x.reps, x.spar, s));
+    if ((st = band_phase_bc(b, x, self, x.counts + self, s)) != CCL_OK) return st;
+    CKN(ncclAllGather(x.counts + self, x.counts, 1, ncclInt32, p->comm, s));
     // D + X3
-    st = band_phase_d(b, off, s);
-    if (st != CCL_OK) return st;
-    CKN(ncclAllGather(b.d_exp, p->d_allexp, 2 * (size_t)W, ncclInt32, p->comm, s));
-    CK(cudaMemcpyAsync(p->allexp.data(), p->d_allexp, sizeof(int32_t) * p->allexp.size(),
-                       cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    std::vector<const int64_t *> akeys(nranks);
-    std::vector<const int32_t *> aexp(nranks);
-    for (int k = 0; k < nranks; k++) {
-        akeys[k] = p->allkeys.data() + 2 * (size_t)W * k;
-        aexp[k] = p->allexp.data() + 2 * (size_t)W * k;
-    }
+    if ((st = band_phase_d(b, x, self, n_components, x.exps + self * slots, s)) != CCL_OK) return st;
+    CKN(ncclAllGather(x.exps + self * slots, x.exps, slots, ncclInt32, p->comm, s));
     // E
-    st = band_phase_e(b, akeys.data(), aexp.data(), nranks, band_labels, s);
-    if (st != CCL_OK) return st;
-    p->total = total;
-    CK(cudaMemcpyAsync(n_components, &p->total, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-    return CCL_OK;
+    return band_phase_e(b, x, band_labels, s);
 }
 
 ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0, int H_total,

@@ -63,8 +63,9 @@ struct Workspace {
     int32_t *ticket;      // [1]               dynamic partition counter
     int32_t *rowexcl;     // [nTy]             labels of earlier tile rows
     // row bands only (null for a whole image):
-    const int32_t *xlab;  // [*]               labels of roots owned by other bands; a node
-                          //                   whose parent is -2-f takes xlab[f]
+    const int32_t *xlab;  // [nb*2W]           exported labels of all bands' boundary slots; a
+                          //                   node whose parent is -2-f takes xlab[f]
+    const int32_t *boff;  // [1]               labels of earlier bands (added to every label)
 };
 
 Geometry make_geometry(int H, int W);
@@ -107,18 +108,29 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
                             cudaStream_t stream, cudaEvent_t *ev);
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev);
-// boff = labels of earlier row bands (0 for a whole image), added to every label.
-cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels, int32_t boff,
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev);
 // Row bands: per-pixel root key / root node of local row `row` (-1 background).
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
                            int32_t *nodes, cudaStream_t stream);
-// gparent[act[i].x] = act[i].y
-cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t stream);
-// Per pixel of local row `row`: the final label if the pixel's root node (from
-// band_row_roots) is still a root after band_apply, else -1.
-cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
-                        int32_t *labels_out, int32_t boff, cudaStream_t stream);
+// Cross-band step (row bands).  Slots: band k's first
+// row then last row, W each, at k*2W.
+// rep[s] = first slot (of this band's 2W) with the same band-local root node;
+// noderep is scratch of noderep_count ints (>= the band's node count).
+cudaError_t band_rep(const int32_t *nodes, int n, int32_t *noderep, size_t noderep_count, int32_t *rep,
+                     cudaStream_t stream);
+// Union-find over all nb*2W slots (keys / reps of every band gathered).
+cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
+                         cudaStream_t stream);
+// Link this band's components whose class starts in another component.
+cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys, const int32_t *spar,
+                      const int32_t *nodes, cudaStream_t stream);
+// *boff = sum of counts of earlier bands; *n_total (if not null) = all.
+cudaError_t band_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
+                         cudaStream_t stream);
+// Global label of the root of each of n boundary slots (-1: not a root).
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out,
+                        int n, cudaStream_t stream);
 // Number of kernel launches run_pipeline makes for this geometry.
 int pipeline_launches(const Geometry &g);
 

@@ -983,7 +983,7 @@ k_label(Geometry g, Workspace ws) {
 // band, whose global label arrived in xlab; labels stored here are band-local,
 // K5 adds the band offset).  One warp per tile, over its border nodes.
 __global__ void __launch_bounds__(256)
-k_fixup(Geometry g, Workspace ws, int32_t boff) {
+k_fixup(Geometry g, Workspace ws) {
     pdl_trigger();
     pdl_wait();
     const int lane = lane_id();
@@ -996,7 +996,7 @@ k_fixup(Geometry g, Workspace ws, int32_t boff) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) == node) continue;
         const int r = gfind_ro(ws.gparent, node);
-        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : ws.xlab[-2 - r] - boff;
+        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
         complab[__ldcg(ws.gnodecomp + node) & 0xFFFF] = lab;
     }
 }
@@ -1007,9 +1007,10 @@ k_fixup(Geometry g, Workspace ws, int32_t boff) {
 // warp is one contiguous 512-byte stretch of the output row.
 constexpr int K5_WARPS = 8;
 __global__ void __launch_bounds__(K5_WARPS * 32, 8)
-k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, int32_t off) {
+k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     pdl_trigger();
     pdl_wait();
+    const int32_t off = ws.boff ? __ldcg(ws.boff) : 0;  // labels of earlier row bands
     __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
     const int lane = lane_id(), wi = threadIdx.x >> 5;
     // warp = one row segment; consecutive warps and CTAs take consecutive
@@ -1102,16 +1103,73 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     }
 }
 
-__global__ void k_band_apply(int32_t *gparent, const int2 *act, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) gparent[act[i].x] = act[i].y;
-}
+// ------------------------------------------------------------ cross-band step
+// Boundary slots: band k's first row then its last row, W slots each, at
+// k*2W.  Every rank holds the keys of all bands' slots (all-gathered) and
+// resolves the cross-band classes itself, identically: a union-find over the
+// slots, joining the slots of one band-local component (via a representative
+// slot) and 8-adjacent pixels across each band boundary, linking the root
+// with the larger key under the smaller, so a class's root is its first pixel
+// in raster order (PARemSP's boundary merge).
 
-__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int32_t boff) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.W) return;
-    const int n = nodes[c];
-    out[c] = (n >= 0 && __ldcg(ws.gparent + n) == n) ? __ldcg(ws.gnodelab + n) + boff : -1;
+// Representative slot of every boundary slot of this band: the first slot
+// whose pixel has the same band-local root node.
+__global__ void k_xb_rep1(const int32_t *nodes, int n, int32_t *noderep) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n && nodes[s] >= 0) atomicMin(noderep + nodes[s], s);
+}
+__global__ void k_xb_rep2(const int32_t *nodes, int n, const int32_t *noderep, int32_t *rep) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) rep[s] = nodes[s] >= 0 ? noderep[nodes[s]] : -1;
+}
+__global__ void k_xb_init(int32_t *spar, int n) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) spar[t] = t;
+}
+__global__ void k_xb_union(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nb * 2 * W || keys[t] < 0) return;
+    const int k = t / (2 * W), s = t % (2 * W);
+    const int r = reps[t];
+    if (r >= 0 && r != s) gunion(spar, keys, t, k * 2 * W + r);
+    if (s >= W && k + 1 < nb) {  // last row of band k against the first row of band k+1
+        const int c = s - W;
+        for (int dc = -1; dc <= 1; dc++) {
+            const int cc = c + dc, t2 = (k + 1) * 2 * W + cc;
+            if (cc >= 0 && cc < W && keys[t2] >= 0) gunion(spar, keys, t, t2);
+        }
+    }
+}
+// This band's components whose class starts elsewhere are linked to it: to
+// the other component's node in this band, or to a foreign slot (-2-slot)
+// whose label arrives with the exported labels.
+__global__ void k_xb_apply(int W, int self, const int64_t *keys, const int32_t *spar, const int32_t *nodes,
+                           int32_t *gparent) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = self * 2 * W + s;
+    if (s >= 2 * W || keys[t] < 0) return;
+    int r = t;
+    while (spar[r] != r) r = spar[r];
+    if (keys[r] == keys[t]) return;  // the class starts with this component
+    gparent[nodes[s]] = r / (2 * W) == self ? nodes[r - self * 2 * W] : -2 - r;
+}
+__global__ void k_xb_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int off = 0, tot = 0;
+    for (int k = 0; k < nb; k++) {
+        if (k < self) off += counts[k];
+        tot += counts[k];
+    }
+    *boff = off;
+    if (n_total) *n_total = tot;
+}
+// Global label of the root of every boundary slot of this band (-1: not a
+// root after the cross-band links).
+__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int n) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int v = nodes[s];
+    out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) + *ws.boff : -1;
 }
 
 // ==================================================================== host
@@ -1196,17 +1254,17 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
     return cudaGetLastError();
 }
 
-cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels, int32_t boff,
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev) {
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_FIXUP);
-    cudaError_t e = launch_pdl(k_fixup, (g.nT + 7) / 8, 256, 0, stream, g, ws, boff);
+    cudaError_t e = launch_pdl(k_fixup, (g.nT + 7) / 8, 256, 0, stream, g, ws);
     if (e != cudaSuccess) return e;
     mark(K_WRITE);
     e = launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0,
-                   stream, g, ws, labels, boff);
+                   stream, g, ws, labels);
     if (e != cudaSuccess) return e;
     mark(K_COUNT);
     return cudaGetLastError();
@@ -1221,7 +1279,7 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
         return e;
     }
     if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev);
-    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, 0, stream, ev);
+    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev);
     return e;
 }
 
@@ -1231,14 +1289,38 @@ cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int6
     return cudaGetLastError();
 }
 
-cudaError_t band_apply(const Workspace &ws, const int2 *act, int n, cudaStream_t stream) {
-    if (n > 0) k_band_apply<<<(n + 255) / 256, 256, 0, stream>>>(ws.gparent, act, n);
+cudaError_t band_rep(const int32_t *nodes, int n, int32_t *noderep, size_t noderep_count, int32_t *rep,
+                     cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(noderep, 0x7f, noderep_count * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    k_xb_rep1<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep);
+    k_xb_rep2<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep, rep);
     return cudaGetLastError();
 }
 
-cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes,
-                        int32_t *labels_out, int32_t boff, cudaStream_t stream) {
-    k_band_export<<<(g.W + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out, boff);
+cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
+                         cudaStream_t stream) {
+    const int n = nb * 2 * W;
+    k_xb_init<<<(n + 255) / 256, 256, 0, stream>>>(spar, n);
+    k_xb_union<<<(n + 255) / 256, 256, 0, stream>>>(nb, W, keys, reps, spar);
+    return cudaGetLastError();
+}
+
+cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys, const int32_t *spar,
+                      const int32_t *nodes, cudaStream_t stream) {
+    k_xb_apply<<<(2 * W + 255) / 256, 256, 0, stream>>>(W, self, keys, spar, nodes, ws.gparent);
+    return cudaGetLastError();
+}
+
+cudaError_t band_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
+                         cudaStream_t stream) {
+    k_xb_offsets<<<1, 32, 0, stream>>>(nb, self, counts, boff, n_total);
+    return cudaGetLastError();
+}
+
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out,
+                        int n, cudaStream_t stream) {
+    k_band_export<<<(n + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out, n);
     return cudaGetLastError();
 }
 
