@@ -1,7 +1,7 @@
 """Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list:
 per kernel launches, total / average time and share of the step.
 usage: python scripts/launch_summary.py LAUNCHES.csv > profiles/rNN_launches_summary.txt"""
-import csv, io, sys
+import csv, io, re, sys
 lines = open(sys.argv[1]).read().splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
 rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
@@ -9,7 +9,7 @@ agg = {}
 for r in rows:
     if r.get("Metric Name") != "gpu__time_duration.sum":
         continue
-    name = r["Kernel Name"].split("(")[0].split("::")[-1]
+    name = re.sub(r"<.*", "", r["Kernel Name"].split("(")[0].split("::")[-1]).replace("void ", "").strip()
     v = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "ns")
     us = v / 1000 if unit in ("nsecond", "ns") else (v if unit in ("usecond", "us") else v * 1000)

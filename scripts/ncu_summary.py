@@ -6,6 +6,7 @@ throughput, occupancy, top stall reasons and the hottest source lines.
 """
 import argparse
 import csv
+import re
 import io
 import json
 import os
@@ -47,7 +48,7 @@ def main():
     hdr, units = rows[0], rows[1]
     summary = {}
     for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+        name = re.sub(r"<.*", "", r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]).replace("void ", "").strip()
         e = {}
         for m, key in METRICS:
             if m in hdr:
