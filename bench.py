@@ -58,6 +58,22 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s earlier measurement on this pool)"
 
 
+def ncu_issue(kernel, workload, sm_mhz=1965.0, sms=148):
+    """Instruction-issue utilisation of a kernel from the committed ncu --set
+    full summary: executed warp instructions / (duration x issue peak = 148 SMs
+    x 4 schedulers x 1 warp-instruction per clock at the SM clock)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            e = json.load(f)[workload][kernel]
+        rate = float(e["warp_inst"]) / (float(e["duration_ms"]) * 1e-3)
+        peak = sms * 4 * sm_mhz * 1e6
+        return {"unit": "warp-instructions/s", "achieved": rate, "peak": peak, "frac": rate / peak,
+                "issue_active_pct": e.get("issue_active_pct"), "source": "profiles/ncu_summary.json (ncu --set full)"}
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernel, workload):
     """dram read+write bytes per launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -320,6 +336,12 @@ def main():
                     "path": {"achieved": ach, "frac": ach / peak, "algorithmic_bytes_per_step": alg,
                              "traffic": sum(tr_all) if all(t is not None for t in tr_all) else None},
                     "kernels": kern}
+        # K1 moves 1 B/px of algorithmic bytes but is bound by instruction
+        # issue (shared-memory union-find, bit-parallel scans): its issue
+        # utilisation is the roofline that binds it
+        iss = ncu_issue(dom, args.workload)
+        if iss is not None:
+            roofline["issue"] = iss
 
     line = {
         "metric": METRIC, "value": value, "unit": "Gpx/s", "n_gpus": ws, "steps": args.steps,
