@@ -24,6 +24,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
 METRIC = "8-conn CCL Gpixel/s on 21600² image at 1/2/4/8 B200; % of HBM roofline"
 WORKLOAD = "c4_voronoi_21600"
 # algorithmic bytes per pixel: 1 B image read + 4 B label write
@@ -45,6 +46,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="skip the C1/C2 single vs batched lines")
+    ap.add_argument("--shard", action="store_true",
+                    help="use the row-band (NCCL) path even on one GPU (tests the multi-GPU code path)")
     return ap.parse_args()
 
 
@@ -184,6 +187,24 @@ def small_images(dev, stream, batch=64, reps=20):
     return res
 
 
+class stdout_to_stderr:
+    """NCCL prints its version banner on stdout at communicator creation (this
+    image sets NCCL_DEBUG=VERSION), which would break the one-JSON-line
+    contract: point file descriptor 1 at stderr while communicators are made."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -238,7 +259,8 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=dev)
 
     img = synth.generate(args.workload)
     H, W = img.shape
@@ -252,21 +274,26 @@ def main():
     n_out = torch.empty(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    if ws == 1:
+    if ws == 1 and not args.shard:
         plan = ccl.Plan(H, W, device=dev)
         step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
         nTx, nTy = (W + 1023) // 1024, (H + 31) // 32
         # mirrors cclb::pipeline_launches: k_border only runs when tiles have neighbours
         launches_per_step = 5 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
     else:
-        uid = ccl.nccl_unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        comm = ccl.NcclComm(obj[0], ws, rank)
+        with stdout_to_stderr():
+            uid = ccl.nccl_unique_id() if rank == 0 else None
+            obj = [uid]
+            if dist:
+                dist.broadcast_object_list(obj, src=0)
+            comm = ccl.NcclComm(obj[0], ws, rank)
         splan = ccl.ShardPlan(bh, W, row0, H, comm)
         step = lambda: splan.label(d_img, out, n_out)  # noqa: E731
         plan = None
-        launches_per_step = None
+        # our kernels per band step (ccl_bands.cu): K1, K2, 2 boundary rows,
+        # 2 slot representatives, 2 slot union-find, link, K3, K3b, offsets,
+        # export, K4, K5 (the 3 NCCL all-gathers are not counted)
+        launches_per_step = 15
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -356,11 +383,11 @@ def main():
 
     # ---- the paper's <= 1 MB regime (C1, C2): one image per call vs a batch
     # of 64 per call (ccl_label_batch), device-resident, CUDA events
-    if ws == 1 and not args.no_small:
+    if ws == 1 and plan is not None and not args.no_small:
         line["small_images"] = small_images(dev, stream)
 
     # ---- end to end through the public API with host buffers (N=1)
-    if ws == 1 and not args.no_e2e:
+    if ws == 1 and plan is not None and not args.no_e2e:
         h_img = torch.from_numpy(img).pin_memory()
         h_lab = torch.empty((H, W), dtype=torch.int32).pin_memory()
         h_n = torch.empty(1, dtype=torch.int32).pin_memory()
