@@ -98,8 +98,9 @@ struct Band {
     Workspace ws;
     void *mem = nullptr;
     int32_t *d_nodes = nullptr;    // 2W band-local root node of each slot (-1 background)
-    int32_t *d_noderep = nullptr;  // scratch: first slot of each node
+    unsigned long long *d_noderep = nullptr;  // scratch: (epoch, first slot) of each node
     size_t noderep_count = 0;
+    uint32_t epoch = 0;              // calls on this band (band_rep's epoch)
     int32_t *d_small = nullptr;    // [0] N_band, [1] band offset
     int band_H = 0, row0 = 0;
 
@@ -161,7 +162,8 @@ ccl_status band_init(Band &b, int band_H, int W, int row0) {
     b.ws = workspace_bind(b.g, b.mem);
     CK(cudaMalloc(&b.d_nodes, sizeof(int32_t) * 2 * W));
     b.noderep_count = (size_t)b.g.nT * b.g.capb;
-    CK(cudaMalloc(&b.d_noderep, sizeof(int32_t) * b.noderep_count));
+    CK(cudaMalloc(&b.d_noderep, sizeof(unsigned long long) * b.noderep_count));
+    CK(cudaMemset(b.d_noderep, 0xFF, sizeof(unsigned long long) * b.noderep_count));
     CK(cudaMalloc(&b.d_small, sizeof(int32_t) * 4));
     b.ws.boff = b.d_small + 1;
     return CCL_OK;
@@ -185,7 +187,7 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
     CK(run_stage_local(b.g, b.ws, img, s, nullptr));
     CK(band_row_roots(b.g, b.ws, 0, keys, b.d_nodes, s));
     CK(band_row_roots(b.g, b.ws, b.band_H - 1, keys + W, b.d_nodes + W, s));
-    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, b.noderep_count, reps, s));
+    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, s));
     return CCL_OK;
 }
 

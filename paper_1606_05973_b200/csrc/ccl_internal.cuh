@@ -116,8 +116,9 @@ cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int6
 // Cross-band step (row bands).  Slots: band k's first
 // row then last row, W each, at k*2W.
 // rep[s] = first slot (of this band's 2W) with the same band-local root node;
-// noderep is scratch of noderep_count ints (>= the band's node count).
-cudaError_t band_rep(const int32_t *nodes, int n, int32_t *noderep, size_t noderep_count, int32_t *rep,
+// noderep: one entry per node of the band, all-ones initially; epoch: a
+// number that grows with every call on the same scratch (starting at 1).
+cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
                      cudaStream_t stream);
 // Union-find over all nb*2W slots (keys / reps of every band gathered).
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,

@@ -1075,8 +1075,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
 // band's forest (after k_border).  One warp per 1024-px row segment.
 __global__ void __launch_bounds__(256)
 k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
-    const int lane = lane_id();
-    const int tx = blockIdx.x * 8 + (threadIdx.x >> 5);
+    __shared__ int32_t s_node[4][MAXRUN];
+    __shared__ int64_t s_key[4][MAXRUN];
+    const int lane = lane_id(), wi = threadIdx.x >> 5;
+    const int tx = blockIdx.x * 4 + wi;
     if (tx >= g.nTx) return;
     const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
     const int gword = tx * WPR + lane;
@@ -1088,18 +1090,22 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * g.maxrun;
     const int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
-    for (int b = 0; b < 32; b++) {
-        const int c = C0 + 32 * lane + b;
-        if (c >= g.W) break;
-        int64_t key = -1;
-        int32_t node = -1;
-        if ((x >> b) & 1u) {
-            const int comp = rc[run_ord(hx, base, b)];
-            node = gfind_ro(ws.gparent, compnode[comp]);
-            key = ws.gkey[node];
-        }
-        keys[c] = key;
-        nodes[c] = node;
+    // root node and key once per run ...
+    for (int k = lane; k < (int)nr; k += 32) {
+        const int node = gfind_ro(ws.gparent, compnode[rc[k]]);
+        s_node[wi][k] = node;
+        s_key[wi][k] = ws.gkey[node];
+    }
+    __syncwarp();
+    // ... then per pixel, lane = pixel within each 32-pixel word (coalesced)
+    for (int c = 0; c < WPR; c++) {
+        const uint32_t xw = __shfl_sync(FULL, x, c), hw = __shfl_sync(FULL, hx, c), bw = __shfl_sync(FULL, base, c);
+        const int col = C0 + 32 * c + lane;
+        if (col >= g.W) continue;
+        const bool fg = (xw >> lane) & 1u;
+        const int ord = (int)bw + __popc(hw & upto(lane)) - 1;
+        keys[col] = fg ? s_key[wi][ord] : -1;
+        nodes[col] = fg ? s_node[wi][ord] : -1;
     }
 }
 
@@ -1114,13 +1120,17 @@ k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
 
 // Representative slot of every boundary slot of this band: the first slot
 // whose pixel has the same band-local root node.
-__global__ void k_xb_rep1(const int32_t *nodes, int n, int32_t *noderep) {
+// noderep entries carry the call's epoch in their high word (stored
+// complemented, so a newer call's entries are smaller and win atomicMin):
+// the scratch never needs clearing.
+__global__ void k_xb_rep1(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < n && nodes[s] >= 0) atomicMin(noderep + nodes[s], s);
+    if (s < n && nodes[s] >= 0)
+        atomicMin(noderep + nodes[s], ((unsigned long long)(0xFFFFFFFFu - epoch) << 32) | (uint32_t)s);
 }
-__global__ void k_xb_rep2(const int32_t *nodes, int n, const int32_t *noderep, int32_t *rep) {
+__global__ void k_xb_rep2(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < n) rep[s] = nodes[s] >= 0 ? noderep[nodes[s]] : -1;
+    if (s < n) rep[s] = nodes[s] >= 0 ? (int32_t)(uint32_t)__ldcg(noderep + nodes[s]) : -1;
 }
 __global__ void k_xb_init(int32_t *spar, int n) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1285,15 +1295,13 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
 
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
                            int32_t *nodes, cudaStream_t stream) {
-    k_band_rows<<<(g.nTx + 7) / 8, 256, 0, stream>>>(g, ws, row, keys, nodes);
+    k_band_rows<<<(g.nTx + 3) / 4, 128, 0, stream>>>(g, ws, row, keys, nodes);
     return cudaGetLastError();
 }
 
-cudaError_t band_rep(const int32_t *nodes, int n, int32_t *noderep, size_t noderep_count, int32_t *rep,
+cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
                      cudaStream_t stream) {
-    cudaError_t e = cudaMemsetAsync(noderep, 0x7f, noderep_count * sizeof(int32_t), stream);
-    if (e != cudaSuccess) return e;
-    k_xb_rep1<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep);
+    k_xb_rep1<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep, epoch);
     k_xb_rep2<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep, rep);
     return cudaGetLastError();
 }
