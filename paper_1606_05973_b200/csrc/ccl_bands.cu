@@ -185,8 +185,7 @@ ccl_status xband_init(XBand &x, int nb, int W) {
 ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, cudaStream_t s) {
     const int W = b.g.W;
     CK(run_stage_local(b.g, b.ws, img, s, nullptr));
-    CK(band_row_roots(b.g, b.ws, 0, keys, b.d_nodes, s));
-    CK(band_row_roots(b.g, b.ws, b.band_H - 1, keys + W, b.d_nodes + W, s));
+    CK(band_row_roots(b.g, b.ws, keys, b.d_nodes, s));
     CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, s));
     return CCL_OK;
 }
@@ -254,6 +253,7 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
         if ((st = band_phase_a(bands[k], img + (size_t)r0[k] * W, x.keys + k * slots, x.reps + k * slots, s)) !=
             CCL_OK)
             return st;
+    CK(band_resolve_init(nbands, W, x.spar, s));
     CK(band_resolve(nbands, W, x.keys, x.reps, x.spar, s));
     // B + C (+ X2)
     for (int k = 0; k < nbands; k++)
@@ -343,6 +343,7 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     // A + X1 (own slots written in place, then gathered)
     ccl_status st = band_phase_a(b, band_img, x.keys + self * slots, x.reps + self * slots, s);
     if (st != CCL_OK) return st;
+    CK(band_resolve_init(p->nranks, p->W, x.spar, s));
     CKN(ncclGroupStart());
     CKN(ncclAllGather(x.keys + self * slots, x.keys, slots, ncclInt64, p->comm, s));
     CKN(ncclAllGather(x.reps + self * slots, x.reps, slots, ncclInt32, p->comm, s));

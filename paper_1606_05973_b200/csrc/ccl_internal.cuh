@@ -110,9 +110,10 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
                             cudaStream_t stream, cudaEvent_t *ev);
 cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev);
-// Row bands: per-pixel root key / root node of local row `row` (-1 background).
-cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
-                           int32_t *nodes, cudaStream_t stream);
+// Row bands: per-pixel root key / root node of the band's first row (keys[0,W),
+// nodes[0,W)) and last row ([W,2W)); -1 for background.
+cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys, int32_t *nodes,
+                           cudaStream_t stream);
 // Cross-band step (row bands).  Slots: band k's first
 // row then last row, W each, at k*2W.
 // rep[s] = first slot (of this band's 2W) with the same band-local root node;
@@ -120,7 +121,9 @@ cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int6
 // number that grows with every call on the same scratch (starting at 1).
 cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
                      cudaStream_t stream);
-// Union-find over all nb*2W slots (keys / reps of every band gathered).
+// Slot union-find: every slot its own root (may run before the gather) ...
+cudaError_t band_resolve_init(int nb, int W, int32_t *spar, cudaStream_t stream);
+// ... then the unions over all nb*2W slots (keys / reps of every band gathered).
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
                          cudaStream_t stream);
 // Link this band's components whose class starts in another component.

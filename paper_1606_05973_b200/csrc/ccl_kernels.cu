@@ -1074,12 +1074,16 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
 // Per pixel of a local row: the key and node of its component's root in the
 // band's forest (after k_border).  One warp per 1024-px row segment.
 __global__ void __launch_bounds__(256)
-k_band_rows(Geometry g, Workspace ws, int row, int64_t *keys, int32_t *nodes) {
+k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
     __shared__ int32_t s_node[4][MAXRUN];
     __shared__ int64_t s_key[4][MAXRUN];
     const int lane = lane_id(), wi = threadIdx.x >> 5;
-    const int tx = blockIdx.x * 4 + wi;
-    if (tx >= g.nTx) return;
+    const int seg = blockIdx.x * 4 + wi;  // the band's first row, then its last
+    if (seg >= 2 * g.nTx) return;
+    const int side = seg / g.nTx, tx = seg % g.nTx;
+    const int row = side ? g.H - 1 : 0;
+    keys += side * g.W;
+    nodes += side * g.W;
     const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
     const int gword = tx * WPR + lane;
     uint32_t x;
@@ -1293,9 +1297,9 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
     return e;
 }
 
-cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int row, int64_t *keys,
-                           int32_t *nodes, cudaStream_t stream) {
-    k_band_rows<<<(g.nTx + 3) / 4, 128, 0, stream>>>(g, ws, row, keys, nodes);
+cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys, int32_t *nodes,
+                           cudaStream_t stream) {
+    k_band_rows<<<(2 * g.nTx + 3) / 4, 128, 0, stream>>>(g, ws, keys, nodes);
     return cudaGetLastError();
 }
 
@@ -1306,10 +1310,15 @@ cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, u
     return cudaGetLastError();
 }
 
+cudaError_t band_resolve_init(int nb, int W, int32_t *spar, cudaStream_t stream) {
+    const int n = nb * 2 * W;
+    k_xb_init<<<(n + 255) / 256, 256, 0, stream>>>(spar, n);
+    return cudaGetLastError();
+}
+
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
                          cudaStream_t stream) {
     const int n = nb * 2 * W;
-    k_xb_init<<<(n + 255) / 256, 256, 0, stream>>>(spar, n);
     k_xb_union<<<(n + 255) / 256, 256, 0, stream>>>(nb, W, keys, reps, spar);
     return cudaGetLastError();
 }
