@@ -83,11 +83,16 @@ PRODUCT_HDRS = [
 def build_product(force=False, verbose_ptxas=False):
     srcs = [os.path.join(ROOT, s) for s in PRODUCT_SRCS]
     deps = srcs + [os.path.join(ROOT, h) for h in PRODUCT_HDRS]
-    out = os.path.join(ROOT, "paper_1606_05973_b200", "libccl_b200.so")
-    if not (force or _stale(out, deps)):
+    # CCL_VARIANT=name CCL_DEFS="-DX=1 ..." builds an experiment variant
+    # libccl_<name>.so (loaded with CCL_B200_LIB=libccl_<name>.so)
+    variant = os.environ.get("CCL_VARIANT", "")
+    defs = os.environ.get("CCL_DEFS", "").split()
+    out = os.path.join(ROOT, "paper_1606_05973_b200",
+                       "libccl_%s.so" % variant if variant else "libccl_b200.so")
+    if not (force or variant or _stale(out, deps)):
         return out
     nccl_inc, nccl_lib = _nccl_dirs()
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" + ("_" + variant if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for s in srcs:
@@ -95,7 +100,7 @@ def build_product(force=False, verbose_ptxas=False):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-rdc=false", "-I", os.path.join(ROOT, "include"),
                "-I", os.path.join(ROOT, "paper_1606_05973_b200", "csrc"),
-               "-I", nccl_inc, "-c", s, "-o", o]
+               "-I", nccl_inc, *defs, "-c", s, "-o", o]
         if verbose_ptxas:
             cmd[1:1] = ["-Xptxas", "-v"]
         _run(cmd)

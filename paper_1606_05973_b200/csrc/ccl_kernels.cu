@@ -427,6 +427,11 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             xs[i] = (r0 + i < rows && gword < g.WW) ? load_word<THR>(img, g, R0 + r0 + i, 32 * gword) : 0u;
     }
     pdl_wait();  // the previous call's kernels are done with the workspace
+    // bm (1/8 B per pixel) is read again by K2 and K5 while ~5 B/px of image
+    // and labels stream through L2: it is stored with the evict_last priority
+    // (K5's label stores are evict_first), measured -10 us on C4
+    uint64_t pol_last;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
     if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
         for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
@@ -434,7 +439,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
 #pragma unroll
     for (int i = 0; i < S; i++) {
         sm.mc[r0 + i][lane] = xs[i];  // raw masks (mc is free until P2a)
-        if (r0 + i < rows && gword < g.WW) ws.bm[(int64_t)(R0 + r0 + i) * g.WW + gword] = xs[i];
+        if (r0 + i < rows && gword < g.WW) {
+            asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(ws.bm + (int64_t)(R0 + r0 + i) * g.WW + gword),
+                         "r"(xs[i]), "l"(pol_last) : "memory");
+        }
     }
     if (lane < S) sm.bcnt[r0 + lane] = 0;
     __syncthreads();
@@ -1041,6 +1049,8 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     }
     __syncwarp();
     int32_t *out = labels + (int64_t)row * g.W + C0;
+    uint64_t pol_first;  // labels are not read again: evict first (bm, runcomp stay in L2)
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
 #pragma unroll
     for (int c = 0; c < 8; c++) {
         const int wsrc = 4 * c + (lane >> 3);  // lane-word holding these 4 pixels
@@ -1060,7 +1070,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
         int v3 = (nib & 8u) ? L : 0;
         const int P = 128 * c + 4 * lane;
         if (g.aligned) {
-            if (P < vcols) *reinterpret_cast<int4 *>(out + P) = make_int4(v0, v1, v2, v3);
+            if (P < vcols) {
+                asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out + P), "r"(v0), "r"(v1),
+                             "r"(v2), "r"(v3), "l"(pol_first) : "memory");
+            }
         } else {
             if (P < vcols) __stcs(out + P, v0);
             if (P + 1 < vcols) __stcs(out + P + 1, v1);
