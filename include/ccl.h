@@ -208,6 +208,12 @@ ccl_status ccl_nccl_comm_create(const uint8_t id[128], int nranks, int rank,
                                 ccl_nccl_comm_t *comm_out);
 ccl_status ccl_nccl_comm_destroy(ccl_nccl_comm_t comm);
 
+/* Development hook (timing experiments; not part of the labeling contract):
+ *   ccl_debug_set(1, stop): truncate K1 after phase `stop` (99 = off); the
+ *     rest of the pipeline is skipped.  ccl_debug_set(2, x): K1 experiment
+ *     bits (1 = no L2 prefetch).  Returns 0, or 1 for an unknown key. */
+int ccl_debug_set(int key, int value);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,8 @@ _L.ccl_label_threshold.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
 _L.ccl_label_threshold.restype = _i
 _L.ccl_plan_set_threshold.argtypes = [_vp, _i]
 _L.ccl_plan_set_threshold.restype = _i
+_L.ccl_debug_set.argtypes = [_i, _i]
+_L.ccl_debug_set.restype = _i
 _L.ccl_label_batch.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
 _L.ccl_label_batch.restype = _i
 _L.ccl_plan_create_batch.argtypes = [_i, _i, _i, ctypes.POINTER(_vp)]

@@ -1018,19 +1018,23 @@ __global__ void __launch_bounds__(K5_WARPS * 32, 8)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     pdl_trigger();
     pdl_wait();
-    const int32_t off = ws.boff ? __ldcg(ws.boff) : 0;  // labels of earlier row bands
-    __shared__ int32_t s_lab[K5_WARPS][MAXRUN];  // final label of each run of the row
+    // s_lab[w][1 + k] = final label of run k of warp w's row (entry 0 and the
+    // two after the last run are read for pixels they do not label)
+    __shared__ int32_t s_lab[K5_WARPS][MAXRUN + 4];
+    __shared__ uint4 s_word[K5_WARPS][32];  // (foreground, run heads, runs before) of each lane-word
     const int lane = lane_id(), wi = threadIdx.x >> 5;
     // warp = one row segment; consecutive warps and CTAs take consecutive
     // segments in raster order, so the stores in flight cover one contiguous
     // stretch of the label image
-    const int64_t seg = (int64_t)blockIdx.x * K5_WARPS + wi;  // (row, tile column)
-    if (seg >= g.nseg) return;
-    const int row = (int)(seg / g.nTx), tx = (int)(seg % g.nTx);
-    const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
+    const uint32_t seg = blockIdx.x * K5_WARPS + wi;  // (row, tile column); nseg < 2^31
+    if (seg >= (uint32_t)g.nseg) return;
+    const int row = (int)(seg / (uint32_t)g.nTx), tx = (int)(seg - (uint32_t)row * (uint32_t)g.nTx);
+    const int ty = row_tile(g, row);
+    const int C0 = tx * TW, tile = ty * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;
-    const uint16_t *rc = ws.runcomp + seg * g.maxrun;
+    const uint16_t *rc = ws.runcomp + (int64_t)seg * g.maxrun;
+    const int32_t off = ws.boff ? __ldcg(ws.boff) : 0;  // labels of earlier row bands
     // the first 32 run -> component entries are loaded beside the masks (most
     // rows have fewer runs), so the label gather is the only dependent load
     const uint32_t rc0 = lane < g.maxrun ? (uint32_t)__ldcs(rc + lane) : 0u;
@@ -1040,40 +1044,54 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
-    int32_t *rowlab = s_lab[wi];
+    int32_t *rowlab = s_lab[wi] + 1;
     {
         const int32_t *complab = ws.complab + (int64_t)tile * g.capc;
         if (lane < (int)nr) rowlab[lane] = complab[rc0] + off;
 #pragma unroll 1
         for (int k = 32 + lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)] + off;
     }
+    s_word[wi][lane] = make_uint4(x, hx, base, 0u);
     __syncwarp();
     int32_t *out = labels + (int64_t)row * g.W + C0;
     uint64_t pol_first;  // labels are not read again: evict first (bm, runcomp stay in L2)
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    const int b0 = 4 * (lane & 7);  // lane's 4 pixels inside lane-word 4c + lane/8
+    const uint32_t m0 = upto(b0);
+    // labels of pixels 128c + 4*lane .. +3.  Heads of the run mask are never
+    // adjacent, so pixels b0+1..b0+3 lie in the run of pixel b0 or one of the
+    // next two: three independent shared loads and selects
+    auto quad = [&](int c, int &v0, int &v1, int &v2, int &v3) {
+        const uint4 t = s_word[wi][4 * c + (lane >> 3)];
+        const uint32_t nib = t.x >> b0, hn = t.y >> b0;
+        const int32_t *rp = rowlab + ((int)t.z + __popc(t.y & m0) - 1);  // run containing (or before) pixel b0
+        const int l0 = rp[0], l1 = rp[1], l2 = rp[2];
+        const int a1 = (hn & 2u) ? l1 : l0;
+        const int a2 = (hn & 6u) ? l1 : l0;
+        const int a3 = (hn & 8u) ? ((hn & 2u) ? l2 : l1) : a2;
+        v0 = (nib & 1u) ? l0 : 0;
+        v1 = (nib & 2u) ? a1 : 0;
+        v2 = (nib & 4u) ? a2 : 0;
+        v3 = (nib & 8u) ? a3 : 0;
+    };
+    if (g.aligned && vcols == TW) {  // interior segment: eight full 512-byte warp stores
 #pragma unroll
+        for (int c = 0; c < 8; c++) {
+            int v0, v1, v2, v3;
+            quad(c, v0, v1, v2, v3);
+            asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out + 128 * c + 4 * lane),
+                         "r"(v0), "r"(v1), "r"(v2), "r"(v3), "l"(pol_first) : "memory");
+        }
+        return;
+    }
+#pragma unroll 1
     for (int c = 0; c < 8; c++) {
-        const int wsrc = 4 * c + (lane >> 3);  // lane-word holding these 4 pixels
-        const int b0 = 4 * (lane & 7);
-        const uint32_t xw = __shfl_sync(FULL, x, wsrc);
-        const uint32_t hw = __shfl_sync(FULL, hx, wsrc);
-        const uint32_t bw = __shfl_sync(FULL, base, wsrc);
-        const uint32_t nib = (xw >> b0) & 0xFu, hn = (hw >> b0) & 0xFu;
-        int ord = (int)bw + __popc(hw & upto(b0)) - 1;  // run containing (or before) pixel b0
-        int L = ord >= 0 ? rowlab[ord] : 0;
-        int v0 = (nib & 1u) ? L : 0;
-        if (hn & 2u) L = rowlab[++ord];
-        int v1 = (nib & 2u) ? L : 0;
-        if (hn & 4u) L = rowlab[++ord];
-        int v2 = (nib & 4u) ? L : 0;
-        if (hn & 8u) L = rowlab[++ord];
-        int v3 = (nib & 8u) ? L : 0;
         const int P = 128 * c + 4 * lane;
+        if (128 * c >= vcols) break;
+        int v0, v1, v2, v3;
+        quad(c, v0, v1, v2, v3);
         if (g.aligned) {
-            if (P < vcols) {
-                asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out + P), "r"(v0), "r"(v1),
-                             "r"(v2), "r"(v3), "l"(pol_first) : "memory");
-            }
+            if (P < vcols) *reinterpret_cast<int4 *>(out + P) = make_int4(v0, v1, v2, v3);
         } else {
             if (P < vcols) __stcs(out + P, v0);
             if (P + 1 < vcols) __stcs(out + P + 1, v1);

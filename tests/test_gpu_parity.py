@@ -127,6 +127,31 @@ def test_determinism_and_plan_reuse():
     assert no == ref[1] and np.array_equal(lo, ref[0])
 
 
+@pytest.mark.parametrize("shape", [(1500, 4100), (64, 1024), (300, 2052)])
+def test_back_to_back_calls_alternating_inputs(shape):
+    """Calls issued back to back on one plan (the kernels of consecutive calls
+    overlap through programmatic dependent launch), two different inputs
+    alternating, no host synchronisation: every call must match the oracle --
+    a kernel reading a table before this call's producer wrote it would label
+    from the previous call's tables."""
+    H, W = shape
+    imgs = [synth.scaled("c3_percolation_8192", H, W), synth.scaled("c4_voronoi_21600", H, W)]
+    refs = [oracle.label(im) for im in imgs]
+    plan = ccl.Plan(H, W)
+    d = [torch.from_numpy(im).cuda() for im in imgs]
+    outs = [torch.empty((H, W), dtype=torch.int32, device="cuda") for _ in range(2)]
+    ns = [torch.empty(1, dtype=torch.int32, device="cuda") for _ in range(2)]
+    snaps = []
+    for it in range(60):
+        k = it % 2
+        plan.label(d[k], outs[k], ns[k])
+        if it % 15 == 14:  # copies on the same stream: ordered after this call only
+            snaps.append((k, outs[k].clone(), ns[k].clone()))
+    torch.cuda.synchronize()
+    for k, lab, n in snaps + [(0, outs[0], ns[0]), (1, outs[1], ns[1])]:
+        assert int(n.item()) == refs[k][1] and np.array_equal(lab.cpu().numpy(), refs[k][0])
+
+
 def test_label_host_end_to_end():
     img = synth.scaled("c4_voronoi_21600", 2000, 3000)
     plan = ccl.Plan(2000, 3000)
