@@ -45,6 +45,12 @@ def lib():
         L.oracle_p_capacity.restype = ctypes.c_int64
         L.ccl_oracle_label.argtypes = [u8p, ctypes.c_int, ctypes.c_int, i32p, i32p]
         L.ccl_oracle_label.restype = ctypes.c_int
+        L.oracle_scan_cclremsp.argtypes = [u8p, ctypes.c_int, ctypes.c_int, i32p, i32p]
+        L.oracle_scan_cclremsp.restype = ctypes.c_int32
+        L.oracle_p_capacity_cclremsp.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.oracle_p_capacity_cclremsp.restype = ctypes.c_int64
+        L.ccl_oracle_label_cclremsp.argtypes = [u8p, ctypes.c_int, ctypes.c_int, i32p, i32p]
+        L.ccl_oracle_label_cclremsp.restype = ctypes.c_int
         _LIB = L
     return _LIB
 
@@ -107,6 +113,35 @@ def canonicalize(lab, nlabels):
     lab = np.ascontiguousarray(lab, dtype=np.int32).copy()
     lib().oracle_canonicalize(_i32(lab), lab.size, nlabels)
     return lab
+
+
+def label_cclremsp(img):
+    """CCLRemSP (the paper's one-line decision-tree variant, PAPER.md:509-554,
+    Fig. 3) + canonical renumbering: a second, independent sequential labeler
+    (SURVEY.md section 8(f) f4).  Returns (labels int32 HxW, N)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    out = np.empty((H, W), dtype=np.int32)
+    n = np.zeros(1, dtype=np.int32)
+    rc = lib().ccl_oracle_label_cclremsp(_u8(img), H, W, _i32(out), _i32(n))
+    if rc != 0:
+        raise ValueError(f"ccl_oracle_label_cclremsp failed with status {rc}")
+    return out, int(n[0])
+
+
+def scan_cclremsp(img):
+    """Scan_CCLRemSP alone: returns (provisional labels, p, count)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    H, W = img.shape
+    lab = np.zeros((H, W), dtype=np.int32)
+    p = np.zeros(int(lib().oracle_p_capacity_cclremsp(H, W)), dtype=np.int32)
+    count = lib().oracle_scan_cclremsp(_u8(img), H, W, _i32(lab), _i32(p))
+    return lab, p, int(count)
+
+
+def label_cclremsp_fnptr():
+    """Raw C function pointer to ccl_oracle_label_cclremsp (exhaustive driver)."""
+    return ctypes.cast(lib().ccl_oracle_label_cclremsp, ctypes.c_void_p).value
 
 
 def label_fnptr():

@@ -17,6 +17,8 @@
  *   O4  relabel       Alg. "ARemSP" labeling phase PAPER.md:826-830
  *   O5  canonicalize  raster-order renumbering (readings A9, A13; BASELINE.json
  *                     "canonical labels (1..N in raster order of first pixel)")
+ *   O6  Scan_CCLRemSP one-line decision-tree scan, PAPER.md:509-554 + Fig. 3
+ *                     (a second, independent sequential variant: SURVEY f4)
  *
  * Readings of the paper (all listed in DESIGN.md "Readings"):
  *   A1  PAPER.md:879 "merge(p,label(a))" has one argument -> merge(p,label(e),label(a))
@@ -26,9 +28,14 @@
  *   A5  odd H: the last row pairs with a virtual all-background g row
  *   A6  count starts at 1; background label 0; p[0]=0
  *   A7  flatten runs i = 1 .. (count-1) = the max label assigned
- *   A8  merge's return value p[root_x] is not relied upon
+ *   A8  merge's return value p[root_x] is not relied upon by ARemSP (CCLRemSP: A18)
  *   A10 a pixel is foreground iff its byte is non-zero
  *   A12 labels are int32; H*W <= INT32_MAX
+ *   A17 CCLRemSP's own listing is missing (an ARemSP listing stands where it
+ *       belongs): its scan is rebuilt from Fig. 3 and the
+ *       copy / new-label definitions
+ *   A18 copy(c,x) stores merge's return value p[root]: a
+ *       member of the merged set, which is all a provisional label needs
  *
  * Parity status: pinned (see tests/test_oracle_pins.py) -- brute-force BFS on
  * every image with h*w <= 20, random images, closed forms, union-find traces
@@ -171,6 +178,84 @@ int32_t oracle_scan_aremsp(const uint8_t *img, int H, int W,
         }
     }
     return count;                                               /* PAPER.md:929 */
+}
+
+/* ------------------------------------------------------------------ */
+/* O6  Scan_CCLRemSP (SURVEY.md section 8(f) f4): the paper's second    */
+/* sequential variant, "CCLRemSP", PAPER.md:509-554 + Fig. 3 (decision  */
+/* tree of CCLLRPC, PAPER.md:581-652).  Its pseudo-code (Alg. RemSP-I)  */
+/* is missing from PAPER.md (reading A17), so the scan is rebuilt from  */
+/* the prose: one image line at a time, forward mask a b c / d e        */
+/* (Fig. 2a, PAPER.md:559-566), and for every object pixel e the tree   */
+/*   b ? copy(b)                                                         */
+/*     : c ? (a ? copy(c,a) : d ? copy(c,d) : copy(c))                   */
+/*         : (a ? copy(a) : d ? copy(d) : new label)                     */
+/* with (PAPER.md:548-554)                                               */
+/*   copy(x)   : label(e) = p[label(x)]                                  */
+/*   copy(c,x) : label(e) = merge(p, label(c), label(x))  (Rem's merge   */
+/*               with splicing, O2'; its return value p[root] is a       */
+/*               member of the merged set, reading A18)                  */
+/*   new label : label(e) = count, p[count] = count, count++.            */
+/* p must hold ceil(H/2)*ceil(W/2) + 2 zero-filled entries (new labels   */
+/* go to pairwise non-adjacent pixels); returns count.                   */
+/* ------------------------------------------------------------------ */
+int32_t oracle_scan_cclremsp(const uint8_t *img, int H, int W,
+                             int32_t *label, int32_t *p)
+{
+    int32_t count = 1;                              /* A6 */
+    p[0] = 0;
+    for (int r = 0; r < H; r++) {
+        for (int c = 0; c < W; c++) {
+            if (!img_at(img, H, W, r, c)) continue;             /* background: label 0 */
+            int a = img_at(img, H, W, r - 1, c - 1);     /* Fig. 2a mask */
+            int b = img_at(img, H, W, r - 1, c);
+            int cc = img_at(img, H, W, r - 1, c + 1);
+            int d = img_at(img, H, W, r, c - 1);
+            if (b) {
+                LBL(r, c) = p[LBL(r - 1, c)];                   /* copy(b) */
+            } else if (cc) {
+                if (a)                                          /* copy(c,a) */
+                    LBL(r, c) = oracle_merge(p, LBL(r - 1, c + 1), LBL(r - 1, c - 1));
+                else if (d)                                     /* copy(c,d) */
+                    LBL(r, c) = oracle_merge(p, LBL(r - 1, c + 1), LBL(r, c - 1));
+                else                                            /* copy(c) */
+                    LBL(r, c) = p[LBL(r - 1, c + 1)];
+            } else if (a) {
+                LBL(r, c) = p[LBL(r - 1, c - 1)];               /* copy(a) */
+            } else if (d) {
+                LBL(r, c) = p[LBL(r, c - 1)];                   /* copy(d) */
+            } else {                                            /* new label */
+                LBL(r, c) = count;
+                p[count] = count;
+                count++;
+            }
+        }
+    }
+    return count;
+}
+
+int64_t oracle_p_capacity_cclremsp(int H, int W)
+{
+    return (int64_t)((H + 1) / 2) * ((W + 1) / 2) + 2;
+}
+
+/* CCLRemSP (scan O6, flatten O3, labeling phase O4) followed by O5. */
+int ccl_oracle_label_cclremsp(const uint8_t *img, int H, int W,
+                              int32_t *labels, int32_t *n_components)
+{
+    if (!img || !labels || !n_components || H < 1 || W < 1) return 1;
+    if ((int64_t)H * W > INT32_MAX) return 2;
+    int64_t n = (int64_t)H * W;
+    int32_t *p = (int32_t *)calloc((size_t)oracle_p_capacity_cclremsp(H, W), sizeof(int32_t));
+    if (!p) return 5;
+    memset(labels, 0, (size_t)n * sizeof(int32_t));
+    int32_t count = oracle_scan_cclremsp(img, H, W, labels, p);     /* O6 */
+    int32_t N = oracle_flatten(p, count - 1);                          /* O3 */
+    oracle_relabel(labels, n, p);                                      /* O4 */
+    free(p);
+    if (oracle_canonicalize(labels, n, N) != 0) return 5;              /* O5 */
+    *n_components = N;
+    return 0;
 }
 
 /* O4  labeling phase, PAPER.md:826-830: label(e) <- p[label(e)] */

@@ -23,6 +23,10 @@ void oracle_relabel(int32_t *label, int64_t n, const int32_t *p);
 /* Raster-order first-occurrence renumbering. */
 int oracle_canonicalize(int32_t *label, int64_t n, int32_t nlabels);
 int64_t oracle_p_capacity(int H, int W);
+/* CCLRemSP's one-line decision-tree scan, PAPER.md:509-554 + Fig. 3. */
+int32_t oracle_scan_cclremsp(const uint8_t *img, int H, int W, int32_t *label, int32_t *p);
+int64_t oracle_p_capacity_cclremsp(int H, int W);
+int ccl_oracle_label_cclremsp(const uint8_t *img, int H, int W, int32_t *labels, int32_t *n_components);
 /* Whole pipeline: scan -> flatten -> relabel -> canonicalize. */
 int ccl_oracle_label(const uint8_t *img, int H, int W, int32_t *labels, int32_t *n_components);
 

@@ -75,12 +75,13 @@ import numpy as np
 sys.path.insert(0, sys.argv[2])
 import pins
 L = ctypes.CDLL(sys.argv[1])
-fn = ctypes.cast(L.ccl_oracle_label, ctypes.c_void_p).value
+sym = sys.argv[3] if len(sys.argv) > 3 else "ccl_oracle_label"
+fn = ctypes.cast(getattr(L, sym), ctypes.c_void_p).value
 bfs = pins.fnptr("pins_bfs_label")
 for (h, w) in [(4, 4), (3, 5), (5, 3), (3, 3)]:
     if pins.exhaustive(fn, bfs, h, w)[0] > 0:
         sys.exit(10)
-f = L.ccl_oracle_label
+f = getattr(L, sym)
 f.argtypes = [ctypes.POINTER(ctypes.c_uint8), ctypes.c_int, ctypes.c_int,
               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
 rng = np.random.default_rng(1606)
@@ -98,10 +99,10 @@ sys.exit(0)
 """
 
 
-def _survives(so):
+def _survives(so, sym="ccl_oracle_label"):
     """0 = passes every pin; anything else (mismatch, crash, hang) = caught."""
     try:
-        r = subprocess.run([sys.executable, "-c", _CHECK, so, os.path.join(ROOT, "tests")],
+        r = subprocess.run([sys.executable, "-c", _CHECK, so, os.path.join(ROOT, "tests"), sym],
                            timeout=120, capture_output=True)
     except subprocess.TimeoutExpired:
         return False
@@ -118,3 +119,36 @@ def test_mutant_is_caught(workdir, name):
     old, new = MUTANTS[name]
     so = _build_mutant(workdir, name, old, new)
     assert not _survives(so), f"mutant {name} survived the oracle pins"
+
+
+# CCLRemSP (O6): slips in the one-line decision-tree scan
+MUTANTS_CCLREMSP = {
+    # copy(c,a) without the merge: keeps c's label only
+    "c_a_no_merge": ("LBL(r, c) = oracle_merge(p, LBL(r - 1, c + 1), LBL(r - 1, c - 1));",
+                     "LBL(r, c) = p[LBL(r - 1, c + 1)];"),
+    # copy(c,d) merges c with a instead of d
+    "c_d_wrong_operand": ("LBL(r, c) = oracle_merge(p, LBL(r - 1, c + 1), LBL(r, c - 1));",
+                          "LBL(r, c) = oracle_merge(p, LBL(r - 1, c + 1), LBL(r - 1, c - 1));"),
+    # the tree tests a before c (copy(a) would then skip c)
+    "tree_a_before_c": ("} else if (cc) {\n                if (a)", "} else if (cc && !a) {\n                if (a)"),
+    # c read at the wrong column (r-1, c-1)
+    "c_wrong_column": ("int cc = img_at(img, H, W, r - 1, c + 1);\n            int d = img_at",
+                       "int cc = img_at(img, H, W, r - 1, c - 1);\n            int d = img_at"),
+    # d read from the row above
+    "d_wrong_row": ("int d = img_at(img, H, W, r, c - 1);", "int d = img_at(img, H, W, r - 1, c - 1);"),
+    # new labels are not made their own parent
+    "new_label_no_parent": ("LBL(r, c) = count;\n                p[count] = count;\n                count++;\n            }\n        }\n    }\n    return count;\n}\n\nint64_t oracle_p_capacity_cclremsp",
+                            "LBL(r, c) = count;\n                count++;\n            }\n        }\n    }\n    return count;\n}\n\nint64_t oracle_p_capacity_cclremsp"),
+}
+
+
+def test_unmutated_cclremsp_passes(workdir):
+    so = _build_mutant(workdir, "identity_ccl", "int32_t k = 1;", "int32_t k = 1;")
+    assert _survives(so, "ccl_oracle_label_cclremsp")
+
+
+@pytest.mark.parametrize("name", sorted(MUTANTS_CCLREMSP))
+def test_cclremsp_mutant_is_caught(workdir, name):
+    old, new = MUTANTS_CCLREMSP[name]
+    so = _build_mutant(workdir, "ccl_" + name, old, new)
+    assert not _survives(so, "ccl_oracle_label_cclremsp"), f"mutant {name} survived the CCLRemSP pins"
