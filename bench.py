@@ -403,6 +403,52 @@ def main():
                        "h2d_bytes_per_step": H * W, "d2h_bytes_per_step": H * W * 4 + 4,
                        "ms_per_step": ems}
 
+    # ---- end to end at N > 1 (or --shard): every rank copies its band in from
+    # pinned host memory, labels it through the sharded API, and reads its
+    # labels and N back; max over ranks of the per-step time
+    if plan is None and not args.no_e2e:
+        h_band = torch.from_numpy(band).pin_memory()
+        h_lab = torch.empty((bh, W), dtype=torch.int32).pin_memory()
+        h_n = torch.empty(1, dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            d_img.copy_(h_band, non_blocking=True)
+            splan.label(d_img, out, n_out)
+            h_lab.copy_(out, non_blocking=True)
+            h_n.copy_(n_out, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = a.elapsed_time(b) / args.e2e_steps
+        if dist:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        line["e2e"] = {"value": H * W / (ems * 1e-3) / 1e9, "unit": "Gpx/s",
+                       "h2d_bytes_per_step": H * W, "d2h_bytes_per_step": H * W * 4 + 4 * ws,
+                       "ms_per_step": ems}
+
+    # ---- parity at N > 1: every rank checks its band of the timed output
+    # against the oracle's labels of the whole image (one flag, max over ranks)
+    if plan is None and result_labels is not None and not args.no_cpu_baseline:
+        import oracle
+        lab_o, n_o = oracle.label(img)
+        bad = int(n_o != n_gpu or not np.array_equal(lab_o[row0:row0 + bh], result_labels))
+        if dist:
+            t = torch.tensor([bad], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bad = int(t.item())
+        line["parity"] = {"vs": "oracle", "bit_exact": bad == 0, "n_components": n_gpu,
+                          "checked": "every rank's band"}
+
     # ---- CPU baseline (the oracle as it stands) + parity of the timed output
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         t, (lab_o, n_o) = time_oracle(img, args.cpu_runs)
