@@ -291,9 +291,10 @@ def main():
         step = lambda: splan.label(d_img, out, n_out)  # noqa: E731
         plan = None
         # our kernels per band step (ccl_bands.cu): K1, K2, boundary rows,
-        # 2 slot representatives, 2 slot union-find, link, K3, K3b, offsets,
-        # export, K4, K5 (the 3 NCCL all-gathers are not counted)
-        launches_per_step = 14
+        # 2 slot representatives (the second also starts the slot union-find),
+        # slot unions, link, K3, K3b, export (+ band offset), K4, K5 (the 3
+        # NCCL all-gathers are not counted)
+        launches_per_step = 12
 
     for _ in range(max(3, args.warmup)):
         step()

@@ -182,11 +182,12 @@ ccl_status xband_init(XBand &x, int nb, int W) {
 }
 
 // A: local labeling; slot keys / nodes / representatives into (keys, reps)
-ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, cudaStream_t s) {
+ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, int32_t *spar, int spar_lo,
+                        int spar_hi, cudaStream_t s) {
     const int W = b.g.W;
     CK(run_stage_local(b.g, b.ws, img, s, nullptr));
     CK(band_row_roots(b.g, b.ws, keys, b.d_nodes, s));
-    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, s));
+    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, spar, spar_lo, spar_hi, s));
     return CCL_OK;
 }
 
@@ -201,8 +202,7 @@ ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, 
 // D: with all counts known, the band offset and the labels of its slots' roots
 ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int32_t *exp_out,
                         cudaStream_t s) {
-    CK(band_offsets(x.nb, self, x.counts, b.d_small + 1, n_total, s));
-    CK(band_export(b.g, b.ws, b.d_nodes, exp_out, 2 * x.W, s));
+    CK(band_export(b.g, b.ws, b.d_nodes, exp_out, 2 * x.W, x.nb, self, x.counts, b.d_small + 1, n_total, s));
     return CCL_OK;
 }
 
@@ -250,10 +250,9 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
     const size_t slots = 2 * (size_t)W;
     // A (+ X1: every band writes its slots straight into the shared tables)
     for (int k = 0; k < nbands; k++)
-        if ((st = band_phase_a(bands[k], img + (size_t)r0[k] * W, x.keys + k * slots, x.reps + k * slots, s)) !=
-            CCL_OK)
+        if ((st = band_phase_a(bands[k], img + (size_t)r0[k] * W, x.keys + k * slots, x.reps + k * slots, x.spar,
+                               (int)(k * slots), (int)((k + 1) * slots), s)) != CCL_OK)
             return st;
-    CK(band_resolve_init(nbands, W, x.spar, s));
     CK(band_resolve(nbands, W, x.keys, x.reps, x.spar, s));
     // B + C (+ X2)
     for (int k = 0; k < nbands; k++)
@@ -341,9 +340,9 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     const size_t slots = 2 * (size_t)p->W;
     const int self = p->rank;
     // A + X1 (own slots written in place, then gathered)
-    ccl_status st = band_phase_a(b, band_img, x.keys + self * slots, x.reps + self * slots, s);
+    ccl_status st = band_phase_a(b, band_img, x.keys + self * slots, x.reps + self * slots, x.spar, 0,
+                                 (int)(p->nranks * slots), s);
     if (st != CCL_OK) return st;
-    CK(band_resolve_init(p->nranks, p->W, x.spar, s));
     CKN(ncclGroupStart());
     CKN(ncclAllGather(x.keys + self * slots, x.keys, slots, ncclInt64, p->comm, s));
     CKN(ncclAllGather(x.reps + self * slots, x.reps, slots, ncclInt32, p->comm, s));

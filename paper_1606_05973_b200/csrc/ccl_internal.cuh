@@ -119,22 +119,20 @@ cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys
 // rep[s] = first slot (of this band's 2W) with the same band-local root node;
 // noderep: one entry per node of the band, all-ones initially; epoch: a
 // number that grows with every call on the same scratch (starting at 1).
+// Also starts the slot union-find: spar[t] = t for t in [spar_lo, spar_hi).
 cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
-                     cudaStream_t stream);
-// Slot union-find: every slot its own root (may run before the gather) ...
-cudaError_t band_resolve_init(int nb, int W, int32_t *spar, cudaStream_t stream);
-// ... then the unions over all nb*2W slots (keys / reps of every band gathered).
+                     int32_t *spar, int spar_lo, int spar_hi, cudaStream_t stream);
+// The unions over all nb*2W slots (keys / reps of every band gathered).
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
                          cudaStream_t stream);
 // Link this band's components whose class starts in another component.
 cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys, const int32_t *spar,
                       const int32_t *nodes, cudaStream_t stream);
+// Global label of the root of each of n boundary slots (-1: not a root);
 // *boff = sum of counts of earlier bands; *n_total (if not null) = all.
-cudaError_t band_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
-                         cudaStream_t stream);
-// Global label of the root of each of n boundary slots (-1: not a root).
-cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out,
-                        int n, cudaStream_t stream);
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
+                        int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
+                        cudaStream_t stream);
 // Number of kernel launches run_pipeline makes for this geometry.
 int pipeline_launches(const Geometry &g);
 

@@ -25,6 +25,7 @@
 //   K5 k_write        labeling phase: every pixel gets its
 //                     component's label; coalesced 16-byte streaming stores.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -1106,6 +1107,8 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
 // band's forest (after k_border).  One warp per 1024-px row segment.
 __global__ void __launch_bounds__(256)
 k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int32_t s_node[4][MAXRUN];
     __shared__ int64_t s_key[4][MAXRUN];
     const int lane = lane_id(), wi = threadIdx.x >> 5;
@@ -1159,19 +1162,24 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
 // complemented, so a newer call's entries are smaller and win atomicMin):
 // the scratch never needs clearing.
 __global__ void k_xb_rep1(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch) {
+    pdl_trigger();
+    pdl_wait();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s < n && nodes[s] >= 0)
         atomicMin(noderep + nodes[s], ((unsigned long long)(0xFFFFFFFFu - epoch) << 32) | (uint32_t)s);
 }
-__global__ void k_xb_rep2(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep) {
+// (also starts the slot union-find: every slot in [lo, hi) its own root)
+__global__ void k_xb_rep2(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep,
+                          int32_t *spar, int lo, int hi) {
+    pdl_trigger();
+    pdl_wait();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s < n) rep[s] = nodes[s] >= 0 ? (int32_t)(uint32_t)__ldcg(noderep + nodes[s]) : -1;
-}
-__global__ void k_xb_init(int32_t *spar, int n) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n) spar[t] = t;
+    if (lo + s < hi) spar[lo + s] = lo + s;
 }
 __global__ void k_xb_union(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nb * 2 * W || keys[t] < 0) return;
     const int k = t / (2 * W), s = t % (2 * W);
@@ -1190,6 +1198,8 @@ __global__ void k_xb_union(int nb, int W, const int64_t *keys, const int32_t *re
 // whose label arrives with the exported labels.
 __global__ void k_xb_apply(int W, int self, const int64_t *keys, const int32_t *spar, const int32_t *nodes,
                            int32_t *gparent) {
+    pdl_trigger();
+    pdl_wait();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     const int t = self * 2 * W + s;
     if (s >= 2 * W || keys[t] < 0) return;
@@ -1198,23 +1208,28 @@ __global__ void k_xb_apply(int W, int self, const int64_t *keys, const int32_t *
     if (keys[r] == keys[t]) return;  // the class starts with this component
     gparent[nodes[s]] = r / (2 * W) == self ? nodes[r - self * 2 * W] : -2 - r;
 }
-__global__ void k_xb_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Global label of the root of every boundary slot of this band (-1: not a
+// root after the cross-band links); the band offset (labels of earlier
+// bands, from the gathered counts) is computed by every thread and stored
+// once for K4/K5, with the total N.
+__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int n, int nb, int self,
+                              const int32_t *counts, int32_t *boff, int32_t *n_total) {
+    pdl_trigger();
+    pdl_wait();
     int off = 0, tot = 0;
     for (int k = 0; k < nb; k++) {
-        if (k < self) off += counts[k];
-        tot += counts[k];
+        const int c = __ldcg(counts + k);
+        off += k < self ? c : 0;
+        tot += c;
     }
-    *boff = off;
-    if (n_total) *n_total = tot;
-}
-// Global label of the root of every boundary slot of this band (-1: not a
-// root after the cross-band links).
-__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int n) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s == 0) {
+        *boff = off;
+        if (n_total) *n_total = tot;
+    }
     if (s >= n) return;
     const int v = nodes[s];
-    out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) + *ws.boff : -1;
+    out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) + off : -1;
 }
 
 // ==================================================================== host
@@ -1330,46 +1345,34 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
 
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys, int32_t *nodes,
                            cudaStream_t stream) {
-    k_band_rows<<<(2 * g.nTx + 3) / 4, 128, 0, stream>>>(g, ws, keys, nodes);
-    return cudaGetLastError();
+    return launch_pdl(k_band_rows, (2 * g.nTx + 3) / 4, 128, 0, stream, g, ws, keys, nodes);
 }
 
 cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
-                     cudaStream_t stream) {
-    k_xb_rep1<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep, epoch);
-    k_xb_rep2<<<(n + 255) / 256, 256, 0, stream>>>(nodes, n, noderep, rep);
-    return cudaGetLastError();
-}
-
-cudaError_t band_resolve_init(int nb, int W, int32_t *spar, cudaStream_t stream) {
-    const int n = nb * 2 * W;
-    k_xb_init<<<(n + 255) / 256, 256, 0, stream>>>(spar, n);
-    return cudaGetLastError();
+                     int32_t *spar, int spar_lo, int spar_hi, cudaStream_t stream) {
+    cudaError_t e = launch_pdl(k_xb_rep1, (n + 255) / 256, 256, 0, stream, nodes, n, noderep, epoch);
+    if (e != cudaSuccess) return e;
+    const int m = std::max(n, spar_hi - spar_lo);
+    return launch_pdl(k_xb_rep2, (m + 255) / 256, 256, 0, stream, nodes, n, (const unsigned long long *)noderep,
+                      rep, spar, spar_lo, spar_hi);
 }
 
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
                          cudaStream_t stream) {
     const int n = nb * 2 * W;
-    k_xb_union<<<(n + 255) / 256, 256, 0, stream>>>(nb, W, keys, reps, spar);
-    return cudaGetLastError();
+    return launch_pdl(k_xb_union, (n + 255) / 256, 256, 0, stream, nb, W, keys, reps, spar);
 }
 
 cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys, const int32_t *spar,
                       const int32_t *nodes, cudaStream_t stream) {
-    k_xb_apply<<<(2 * W + 255) / 256, 256, 0, stream>>>(W, self, keys, spar, nodes, ws.gparent);
-    return cudaGetLastError();
+    return launch_pdl(k_xb_apply, (2 * W + 255) / 256, 256, 0, stream, W, self, keys, spar, nodes, ws.gparent);
 }
 
-cudaError_t band_offsets(int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
-                         cudaStream_t stream) {
-    k_xb_offsets<<<1, 32, 0, stream>>>(nb, self, counts, boff, n_total);
-    return cudaGetLastError();
-}
-
-cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out,
-                        int n, cudaStream_t stream) {
-    k_band_export<<<(n + 255) / 256, 256, 0, stream>>>(g, ws, nodes, labels_out, n);
-    return cudaGetLastError();
+cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
+                        int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
+                        cudaStream_t stream) {
+    return launch_pdl(k_band_export, (n + 255) / 256, 256, 0, stream, g, ws, nodes, labels_out, n, nb, self, counts,
+                      boff, n_total);
 }
 
 }  // namespace cclb
