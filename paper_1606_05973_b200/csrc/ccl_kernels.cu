@@ -500,8 +500,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         // upper row: heads and run-index base of lanes lane-1, lane, lane+1
         const uint32_t hu = u & ~((u << 1) | (up >> 31));
         const int ub = kidx(rl - 1, sm.hbase[rl - 1][lane]);
-        const uint32_t hup = __shfl_up_sync(FULL, hu, 1), hun = __shfl_down_sync(FULL, hu, 1);
-        const int ubp = __shfl_up_sync(FULL, ub, 1), ubn = __shfl_down_sync(FULL, ub, 1);
+        const uint32_t hun = __shfl_down_sync(FULL, hu, 1);
         const uint32_t uL = (u << 1) | (up >> 31);  // upper pixel at p-1
         const uint32_t t = x & (u | uL | (u >> 1) | (un << 31));
         const uint32_t s = smear_up(t, x);
@@ -514,18 +513,16 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         sm.mc[rl][lane] = mc;
         const int lbase = kidx(rl, sm.hbase[rl][lane]) - 1;
         const bool instrip = i > 0;
+        // upper heads of this word and the next word's first pixel, so the
+        // run of the upper pixel q in [-1, 32] is ub - 1 + (heads at <= q)
+        const uint64_t hu64 = (uint64_t)hu | ((uint64_t)(hun & 1u) << 32);
+        const uint32_t uLu = uL | u;
         while (ft) {
             const int b = __ffs(ft) - 1;
             ft &= ft - 1;
-            // leftmost upper foreground pixel among p-1, p, p+1 and its run
-            int ui;
-            if ((uL >> b) & 1u) {
-                ui = b == 0 ? ubp + __popc(hup) - 1 : ub + __popc(hu & upto(b - 1)) - 1;
-            } else if ((u >> b) & 1u) {
-                ui = ub + __popc(hu & upto(b)) - 1;
-            } else {
-                ui = b == 31 ? ubn + (int)(hun & 1u) - 1 : ub + __popc(hu & upto(b + 1)) - 1;
-            }
+            // leftmost upper foreground pixel q among p-1, p, p+1 (q+1 = b, b+1, b+2)
+            const int q1 = b + 2 - (int)((uL >> b) & 1u) - (int)((uLu >> b) & 1u);
+            const int ui = ub - 1 + __popcll(hu64 & ((1ull << q1) - 1ull));
             vp[lbase + __popc(hx & upto(b))] = instrip ? vp[ui] : (uint16_t)ui;
         }
         __syncwarp();
@@ -553,7 +550,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             m &= m - 1;
             const int a = ub + __popc(hu & upto(b)) - 1;  // the upper run with head h
             // the lower run containing pixel h-1
-            const int c = b == 0 ? xb - 1 : xb + __popc(hx & upto(b - 1)) - 1;
+            const int c = xb - 1 + __popc(hx & ((1u << b) - 1u));
             if (vp[a] != vp[c]) merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
         }
     }
