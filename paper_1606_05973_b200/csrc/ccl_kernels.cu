@@ -630,7 +630,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
-        const int rf = __shfl_sync(FULL, rowfirst, rl);
         int bi = __shfl_sync(FULL, bfirst, rl);
         const bool hasb = sm.bcnt[rl] != 0;
         const uint32_t *brow = bbits + rl * WPR;
