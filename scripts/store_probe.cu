@@ -168,6 +168,54 @@ __global__ void __launch_bounds__(WARPS * 32) k_seg_pipe(int32_t *out, const uin
     }
 }
 
+
+// Warp-specialized: producer warps load (dependent) and build each segment's
+// labels in shared memory (double buffer); paired consumer warps only copy
+// shared -> global with 16-B register stores.  Persistent CTAs.
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+template <int NP>
+__global__ void __launch_bounds__(NP * 64) k_ws(int32_t *out, const uint32_t *src) {
+    __shared__ __align__(16) int32_t buf[NP][1024];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool prod = w < NP;
+    const int pair = prod ? w : w - NP;
+    const uint32_t nseg = (uint32_t)H * NTX;
+    const uint32_t stride = gridDim.x * NP;
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int32_t *b = buf[pair];
+    // lockstep pairs: both warps pass both barriers every iteration (no
+    // deadlock); the producer's next load overlaps the consumer's stores
+    for (uint32_t seg = blockIdx.x * NP + pair; seg < nseg; seg += stride) {
+        if (prod) {
+            const uint32_t v = __ldcg(src + (uint64_t)seg * 32 + lane);
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int a = __shfl_sync(0xffffffffu, (int)v, 4 * c + (lane >> 3));
+                *reinterpret_cast<int4 *>(b + 128 * c + 4 * lane) = make_int4(a, (int)seg, c, 1);
+            }
+        }
+        nb_sync(1 + 2 * pair, 64);
+        int4 r[8];
+        if (!prod) {
+#pragma unroll
+            for (int c = 0; c < 8; c++) r[c] = *reinterpret_cast<const int4 *>(b + 128 * c + 4 * lane);
+        }
+        nb_sync(2 + 2 * pair, 64);
+        if (!prod) {
+            const int row = (int)(seg / NTX), tx = (int)(seg - (uint32_t)row * NTX);
+            const int C0 = tx * TW, vcols = min(TW, W - C0);
+            int32_t *o = out + (int64_t)row * W + C0;
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int P = 128 * c + 4 * lane;
+                if (P < vcols) st4(o + P, r[c].x, r[c].y, r[c].z, r[c].w, pol, 1);
+            }
+        }
+    }
+}
+
 int main() {
     int32_t *out;
     cudaMalloc(&out, (size_t)H * W * 4);
@@ -214,10 +262,20 @@ int main() {
         snprintf(nm, sizeof nm, "dep, 4 seg/warp il %d", il);
         run(nm, [&] { k_seg_depn<4, 8><<<(unsigned)((nseg + 31) / 32), 256>>>(out, src, il); });
     }
-    for (int cps : {4, 8, 16}) {
+    for (int cps : {4, 8}) {
         char nm[80];
         snprintf(nm, sizeof nm, "dep, persistent pipelined %d CTA/SM", cps);
         run(nm, [&] { k_seg_pipe<8><<<148 * cps, 256>>>(out, src); });
+    }
+    for (int cps : {2, 4, 8}) {
+        char nm[80];
+        snprintf(nm, sizeof nm, "dep, warp-specialized 4+4 warps, %d CTA/SM", cps);
+        run(nm, [&] { k_ws<4><<<148 * cps, 256>>>(out, src); });
+    }
+    for (int cps : {2, 4, 6}) {
+        char nm[80];
+        snprintf(nm, sizeof nm, "dep, warp-specialized 5+5 warps, %d CTA/SM", cps);
+        run(nm, [&] { k_ws<5><<<148 * cps, 320>>>(out, src); });
     }
     for (int dep = 0; dep < 0; dep++) {
         {

@@ -69,6 +69,22 @@ def test_structured_edge_cases():
         assert_same(img, "hstripes")
 
 
+@pytest.mark.parametrize("H,W", [(1 << 21, 1), (1 << 20, 3), (2, (1 << 20) + 5), (3, 3 * 1024 * 1024 + 17)])
+def test_extreme_aspect_ratios(H, W):
+    """Very tall (65536 tile rows: the numbering scan's longest lookback chain)
+    and very wide (3073 tile columns in one tile row: the longest segment
+    scan and the most vertical tile edges per row) images."""
+    for p in (0.5, 0.9):
+        assert_same(synth.bernoulli(H, W, p, seed=H + W), f"aspect p={p}")
+    if W > 3:
+        assert_same(synth.comb(H, W), "comb")
+    else:
+        img = np.zeros((H, W), np.uint8)
+        img[:, 0] = 1
+        img[::1000, 0] = 0  # a column cut every 1000 rows: 2098 components
+        assert_same(img, "cut column")
+
+
 def test_nonbinary_bytes():
     rng = np.random.default_rng(9)
     img = (rng.integers(1, 256, size=(300, 2100)) * (rng.random((300, 2100)) < 0.45)).astype(np.uint8)
