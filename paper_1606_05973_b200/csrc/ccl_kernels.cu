@@ -324,11 +324,12 @@ struct K1Smem {
     // the roots of components that touch the tile border (run k = r*MAXRUN+o
     // -> word [r][o/32], so every warp clears exactly the words it read)
     uint32_t mc[TH][WPR];
-    uint16_t hbase[TH][WPR];       // runs whose head lies in earlier words of the row
+    // P0b-P2b: runs whose head lies in earlier words of the row; P4 on:
+    // node number of the first border root of each 32-run chunk of the row
+    uint16_t hbase[TH][WPR];
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t bcnt[TH];              // border components whose root run lies in the row
-    int32_t rowfirst[TH];          // components whose root run lies in earlier rows
 };
 
 __device__ __forceinline__ int kidx(int r, int o) { return r * MAXRUN + o; }
@@ -619,13 +620,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
-    if (w == 0) sm.rowfirst[lane] = rowfirst;
-    auto comp_of = [&](int k) -> int {  // after the barrier below
-        const uint32_t pk = sm.p[k];
-        const int r = (pk & 0x8000u) ? k : (int)pk;
-        const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
-        return sm.rowfirst[r / MAXRUN] + (int)(pr & 0x1FFu);
-    };
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
@@ -645,6 +639,9 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
                 if (pk & 0x8000u) comprow[c] = (uint8_t)rl;
             }
             if (hasb) {
+                // node number of the chunk's first border root, for P4c
+                // (hbase is free after P2b)
+                if (lane == 0) sm.hbase[rl][o0 >> 5] = (uint16_t)bi;
                 const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
                 const uint32_t bbal = __ballot_sync(FULL, broot);
                 if (broot) {
@@ -660,17 +657,25 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     }
     __syncthreads();
     if (stop <= 4) return;
-    // ---- P4c: nodes of the border pixels (for K2)
+    // ---- P4c: nodes of the border pixels (for K2).  A border run's root r is
+    // a border root; its node is the chunk's first node number (P4) plus the
+    // border roots before it in its bitmap word -- all in shared memory.
     {
+        auto node_of = [&](int k) -> int {
+            const uint32_t pk = sm.p[k];
+            const int r = (pk & 0x8000u) ? k : (int)pk;
+            const int rr = r / MAXRUN, ro = r % MAXRUN;
+            return nodebase + sm.hbase[rr][ro >> 5] + __popc(bbits[rr * WPR + (ro >> 5)] & ((1u << (ro & 31)) - 1u));
+        };
         const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
         for (int o = threadIdx.x; o < ntop; o += NW * 32)
-            ws.topnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(kidx(0, o))];
+            ws.topnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(0, o));
         for (int o = threadIdx.x; o < nbot; o += NW * 32)
-            ws.botnode[(int64_t)tile * g.maxrun + o] = compnode[comp_of(kidx(rows - 1, o))];
+            ws.botnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(rows - 1, o));
         for (int r = threadIdx.x; r < rows; r += NW * 32) {
             const int64_t off = (int64_t)tx * g.H + R0 + r;
-            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? compnode[comp_of(kidx(r, 0))] : -1;
-            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? compnode[comp_of(kidx(r, sm.nrun[r] - 1))] : -1;
+            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? node_of(kidx(r, 0)) : -1;
+            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? node_of(kidx(r, sm.nrun[r] - 1)) : -1;
         }
     }
     int32_t *meta = ws.meta + (int64_t)tile * META;
