@@ -317,6 +317,7 @@ __device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *
 // labels, so "link to the smaller index" keeps every root at its component's
 // first pixel.  Every warp owns S consecutive rows (a strip); per-run work is
 // done a row at a time with lane = run ordinal.
+constexpr int MLCAP = 256;  // P2a -> P2b merge list entries (the rest stay in mc)
 struct K1Smem {
     uint16_t p[RCAP];              // parent of each run (the union-find array p of Alg. merge)
     uint32_t bm[TH][WPR];          // run masks (foreground + filled holes)
@@ -330,6 +331,8 @@ struct K1Smem {
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t bcnt[TH];              // border components whose root run lies in the row
+    uint32_t mlist[MLCAP];         // P2a -> P2b: merge pairs (upper run | lower run << 16)
+    int32_t nmerge;
 };
 
 __device__ __forceinline__ int kidx(int r, int o) { return r * MAXRUN + o; }
@@ -447,6 +450,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         }
     }
     if (lane < S) sm.bcnt[r0 + lane] = 0;
+    if (threadIdx.x == 0) sm.nmerge = 0;
     __syncthreads();
     if (stop < 0) return;
     // ---- P0b: run mask = foreground + bridged single-pixel holes (a background
@@ -511,8 +515,20 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
         uint32_t mc = upper_merge_heads(hu, u, up, x, xp, S_);
         if (rl >= 2) mc &= ~hole_bridged(u, up, sm.bm[rl - 2][lane]);
-        sm.mc[rl][lane] = mc;
         const int lbase = kidx(rl, sm.hbase[rl][lane]) - 1;
+        // the row's merges go to a tile-wide list that all threads work
+        // through in P2b (balanced); what does not fit stays in mc
+        if (mc) {
+            int idx = atomicAdd(&sm.nmerge, __popc(mc));
+            while (mc && idx < MLCAP) {
+                const int b = __ffs(mc) - 1;
+                const int a = ub + __popc(hu & upto(b)) - 1;         // the upper run with head h
+                const int c = lbase + __popc(hx & ((1u << b) - 1u));  // the lower run containing h-1
+                sm.mlist[idx++] = (uint32_t)a | ((uint32_t)c << 16);
+                mc &= mc - 1;
+            }
+        }
+        sm.mc[rl][lane] = mc;
         const bool instrip = i > 0;
         // upper heads of this word and the next word's first pixel, so the
         // run of the upper pixel q in [-1, 32] is ub - 1 + (heads at <= q)
@@ -534,6 +550,16 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // (the decision tree's copy(c,a)/copy(c,d) merges).  The
     // parent chains may still cross strips (a strip's first row points into
     // the strip above): Rem's algorithm works on any forest with p[x] <= x.
+    // The tile's merge list is shared out over all 256 threads (a strip with
+    // many merges no longer holds the barrier); rows whose merges did not fit
+    // in the list finish them per lane below.
+    {
+        const int nm = min(sm.nmerge, MLCAP);
+        for (int i = threadIdx.x; i < nm; i += NW * 32) {
+            const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
+            if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
+        }
+    }
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
