@@ -397,7 +397,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             const int pty = pt / g.nTx;
             const int prow = (BATCH ? tile_r0(g, pty) : pty * TH) + (threadIdx.x >> 3);
             const int pcol = (pt % g.nTx) * TW + (threadIdx.x & 7) * 128;
-            if ((BATCH ? (int)(threadIdx.x >> 3) < tile_rows(g, pty) : prow < g.H) && pcol < g.W) {
+            if ((int)(threadIdx.x >> 3) < TH && (BATCH ? (int)(threadIdx.x >> 3) < tile_rows(g, pty) : prow < g.H) &&
+                pcol < g.W) {
                 const uint8_t *a = img + (int64_t)prow * g.W + pcol;
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
                 if ((threadIdx.x & 7) == 7 && pcol + 127 < g.W)
