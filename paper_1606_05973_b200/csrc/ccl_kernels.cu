@@ -971,8 +971,46 @@ k_label(Geometry g, Workspace ws) {
     uint32_t *bits = sm.nrbits[w];
     uint16_t *wpre = sm.wpre[w];
     int32_t *rb = sm.rbase[w];
+    int32_t *nrrow = sm.nrrow[w];
     const int nodebase = tile * g.capb;
-    kn_nonroots(ws, nodebase, nborder, bits, nbw, sm.nrrow[w], true);
+    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+    const uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
+    // every independent load of the tile at once: the parent and (row,
+    // component) of up to KL_NODES border nodes per lane and the root rows
+    // of the first 4*32 components
+    constexpr int KL_NODES = 4;
+    int par[KL_NODES], gcv[KL_NODES];
+#pragma unroll
+    for (int t = 0; t < KL_NODES; t++) {
+        const int j = lane + 32 * t;
+        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : 0;
+        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+    }
+    uint32_t rr[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) rr[u] = lane + 32 * u < ncomp ? __ldcg(comprow + lane + 32 * u) : 0u;
+    // non-root border components (bits) and their count per row
+    for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
+    nrrow[lane] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < KL_NODES; t++) {
+        const int j = lane + 32 * t;
+        if (j < nborder && par[t] != nodebase + j) {
+            const int c = gcv[t] & 0xFFFF;
+            atomicOr(bits + (c >> 5), 1u << (c & 31));
+            atomicAdd(nrrow + (gcv[t] >> 16), 1);
+        }
+    }
+    for (int j = lane + 32 * KL_NODES; j < nborder; j += 32) {
+        const int node = nodebase + j;
+        if (__ldcg(ws.gparent + node) != node) {
+            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
+            atomicOr(bits + (c >> 5), 1u << (c & 31));
+            atomicAdd(nrrow + (gc >> 16), 1);
+        }
+    }
+    __syncwarp();
     for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
         const int j = j0 + lane;
         const uint32_t pc = j < nbw ? __popc(bits[j]) : 0u;
@@ -983,7 +1021,7 @@ k_label(Geometry g, Workspace ws) {
     }
     {
         uint32_t tot;
-        const int nrp = (int)warp_excl_scan((uint32_t)sm.nrrow[w][lane], tot);
+        const int nrp = (int)warp_excl_scan((uint32_t)nrrow[lane], tot);
         // label(c) = excl + segoff + (roots before c in the tile) - (roots
         // in earlier rows) + 1, roots before c = c - nonroots before c
         rb[lane] = excl + so - (f - nrp) + 1;
@@ -992,13 +1030,12 @@ k_label(Geometry g, Workspace ws) {
     auto nonroots_before = [&](int c) -> int {
         return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
     };
-    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-    const uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
     // four components per lane in flight
     for (int c0 = lane; c0 < ncomp; c0 += 128) {
-        uint32_t rr[4];
+        if (c0 != lane) {
 #pragma unroll
-        for (int u = 0; u < 4; u++) rr[u] = c0 + 32 * u < ncomp ? __ldcg(comprow + c0 + 32 * u) : 0u;
+            for (int u = 0; u < 4; u++) rr[u] = c0 + 32 * u < ncomp ? __ldcg(comprow + c0 + 32 * u) : 0u;
+        }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int c = c0 + 32 * u;
@@ -1006,7 +1043,16 @@ k_label(Geometry g, Workspace ws) {
             complab[c] = rb[rr[u]] + c - nonroots_before(c);
         }
     }
-    for (int j = lane; j < nborder; j += 32) {
+    // labels of the root nodes
+#pragma unroll
+    for (int t = 0; t < KL_NODES; t++) {
+        const int j = lane + 32 * t;
+        if (j < nborder && par[t] == nodebase + j) {
+            const int gc = gcv[t], c = gc & 0xFFFF;
+            ws.gnodelab[nodebase + j] = rb[gc >> 16] + c - nonroots_before(c);
+        }
+    }
+    for (int j = lane + 32 * KL_NODES; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) != node) continue;
         const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
