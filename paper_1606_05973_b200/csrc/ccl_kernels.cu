@@ -842,10 +842,26 @@ struct KNSmem {
 __device__ __forceinline__ void kn_nonroots(const Workspace &ws, int nodebase, int nborder,
                                             uint32_t *bits, int nbw, int32_t *nrrow, bool setbits) {
     const int lane = lane_id();
+    // the parents and (row, component) of 4 nodes per lane are loaded at once
+    int par[4], gcv[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        const int j = lane + 32 * t;
+        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
+        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+    }
     for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
     nrrow[lane] = 0;
     __syncwarp();
-    for (int j = lane; j < nborder; j += 32) {
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        if (par[t] != nodebase + lane + 32 * t) {
+            const int c = gcv[t] & 0xFFFF;
+            if (setbits) atomicOr(bits + (c >> 5), 1u << (c & 31));
+            atomicAdd(nrrow + (gcv[t] >> 16), 1);
+        }
+    }
+    for (int j = lane + 128; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) != node) {
             const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
@@ -1084,7 +1100,22 @@ k_fixup(Geometry g, Workspace ws) {
     const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
     const int nodebase = tile * g.capb;
     int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-    for (int j = lane; j < nborder; j += 32) {
+    // the parents and components of 4 nodes per lane are loaded at once
+    int par[4], gcv[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        const int j = lane + 32 * t;
+        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
+        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
+        const int r = par[t] < 0 ? par[t] : gfind_ro(ws.gparent, par[t]);
+        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
+        st_keep(complab + (gcv[t] & 0xFFFF), lab);
+    }
+    for (int j = lane + 128; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) == node) continue;
         const int r = gfind_ro(ws.gparent, node);
