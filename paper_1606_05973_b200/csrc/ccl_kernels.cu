@@ -787,19 +787,23 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     // crossing the edge repeats its pair on every row it spans
     const int64_t t = (int64_t)(gw - nh_warps) * 32 + lane;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    int tx = 0, r = 0, a = -1, b = -1;
-    const int32_t *L = nullptr;
+    int tx = 0, r = 0, a = -1, b = -1, bu = -1, bd = -1;
     if (t < nv) {
         tx = 1 + (int)(t / g.H);
         r = (int)(t % g.H);
+    }
+    // rows r-1 / r+1 of the same image (a batch stacks images: no edges across)
+    const bool has_up = r % g.IH != 0, has_dn = r + 1 < g.H && (r + 1) % g.IH != 0;
+    if (t < nv) {  // the four node loads of the lane at once
+        const int32_t *L = ws.leftnode + (int64_t)tx * g.H;
         a = ws.rightnode[(int64_t)(tx - 1) * g.H + r];
-        L = ws.leftnode + (int64_t)tx * g.H;
-        if (a >= 0) b = L[r];
+        const int bs = L[r];
+        if (has_up) bu = L[r - 1];
+        if (has_dn) bd = L[r + 1];
+        b = a >= 0 ? bs : -1;
     }
     const int ap = __shfl_up_sync(FULL, a, 1), bp = __shfl_up_sync(FULL, b, 1);
     const int an = __shfl_down_sync(FULL, a, 1), bn = __shfl_down_sync(FULL, b, 1);
-    // rows r-1 / r+1 of the same image (a batch stacks images: no edges across)
-    const bool has_up = r % g.IH != 0, has_dn = r + 1 < g.H && (r + 1) % g.IH != 0;
     const bool up_ok = lane > 0 && has_up;   // lane-1 is row r-1 of this edge
     const bool dn_ok = lane < 31 && has_dn;  // lane+1 is row r+1 of this edge
     if (a < 0) return;
@@ -809,14 +813,8 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         return;
     }
     // diagonal neighbours; skipped when the adjacent row makes the same union
-    if (has_up) {
-        const int bu = L[r - 1];
-        if (bu >= 0 && !(up_ok && ap == a && bp == bu)) gunion(ws.gparent, ws.gkey, a, bu);
-    }
-    if (has_dn) {
-        const int bd = L[r + 1];
-        if (bd >= 0 && !(dn_ok && an == a && bn == bd)) gunion(ws.gparent, ws.gkey, a, bd);
-    }
+    if (bu >= 0 && !(up_ok && ap == a && bp == bu)) gunion(ws.gparent, ws.gkey, a, bu);
+    if (bd >= 0 && !(dn_ok && an == a && bn == bd)) gunion(ws.gparent, ws.gkey, a, bd);
 }
 
 // ========================================================================= K3
