@@ -1053,18 +1053,19 @@ k_label(Geometry g, Workspace ws) {
     auto nonroots_before = [&](int c) -> int {
         return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
     };
-    // four components per lane in flight
+    // four components per lane in flight, the next four loading meanwhile
     for (int c0 = lane; c0 < ncomp; c0 += 128) {
-        if (c0 != lane) {
+        uint32_t rn[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) rr[u] = c0 + 32 * u < ncomp ? __ldcg(comprow + c0 + 32 * u) : 0u;
-        }
+        for (int u = 0; u < 4; u++) rn[u] = c0 + 128 + 32 * u < ncomp ? __ldcg(comprow + c0 + 128 + 32 * u) : 0u;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int c = c0 + 32 * u;
             if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
             st_keep(complab + c, rb[rr[u]] + c - nonroots_before(c));
         }
+#pragma unroll
+        for (int u = 0; u < 4; u++) rr[u] = rn[u];
     }
     // labels of the root nodes
 #pragma unroll
