@@ -736,6 +736,9 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     pdl_trigger();
     pdl_wait();
     __shared__ uint32_t shd[8][2][WPR], sbs[8][2][WPR];
+    constexpr int PCAP = 128;
+    __shared__ uint32_t plist[8][PCAP];  // the edge's unions: (upper run, lower run) ordinals
+    __shared__ int pcnt[8];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * 8 + wib;
     if (gw < nh_warps) {
@@ -751,15 +754,23 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         __syncwarp();
         const int32_t *bot = ws.botnode + (int64_t)((ty - 1) * g.nTx + tx) * g.maxrun;
         const int32_t *top = ws.topnode + (int64_t)(ty * g.nTx + tx) * g.maxrun;
+        if (lane == 0) pcnt[wib] = 0;
+        __syncwarp();
+        // the edge's unions are listed first (run ordinals, shared memory
+        // only) and then done one per lane: a lane with several edges no
+        // longer runs their global union chains one after another
+        auto add = [&](int ou, int ox) {
+            const int i = atomicAdd(&pcnt[wib], 1);
+            if (i < PCAP) plist[wib][i] = (uint32_t)ou | ((uint32_t)ox << 16);
+            else gunion(ws.gparent, ws.gkey, bot[ou], top[ox]);  // list full
+        };
         uint32_t m = first_in_run(x & dilate(U), x);
         while (m) {
             int b = __ffs(m) - 1;
             m &= m - 1;
             int q = 32 * lane + b + leftmost3(u, U.xp, U.xn, b);
             int lq = q >> 5;
-            int nu = bot[run_ord(shd[wib][0][lq], sbs[wib][0][lq], q & 31)];
-            int nx = top[run_ord(X.hx, X.base, b)];
-            gunion(ws.gparent, ws.gkey, nu, nx);
+            add(run_ord(shd[wib][0][lq], sbs[wib][0][lq], q & 31), run_ord(X.hx, X.base, b));
         }
         // upper runs whose leftmost lower neighbour has another leftmost upper
         // neighbour (see upper_merge_heads / hole_bridged in K1)
@@ -776,9 +787,13 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             m &= m - 1;
             int q = 32 * lane + b - 1;  // lower pixel h-1
             int lq = q >> 5;
-            int nx = top[run_ord(shd[wib][1][lq], sbs[wib][1][lq], q & 31)];
-            int nu = bot[run_ord(U.hx, U.base, b)];
-            gunion(ws.gparent, ws.gkey, nu, nx);
+            add(run_ord(U.hx, U.base, b), run_ord(shd[wib][1][lq], sbs[wib][1][lq], q & 31));
+        }
+        __syncwarp();
+        const int np = min(pcnt[wib], PCAP);
+        for (int i = lane; i < np; i += 32) {
+            const uint32_t e = plist[wib][i];
+            gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
         }
         return;
     }
