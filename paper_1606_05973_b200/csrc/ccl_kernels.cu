@@ -252,6 +252,15 @@ __device__ __forceinline__ uint32_t pack8(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t pack16(uint4 v) {
     return pack8(v.x, v.y) | (pack8(v.z, v.w) << 8);
 }
+// The same for bytes known to be 0 or 1 (binary images stored as 0/1): the
+// bytes' low bits go straight into the gather multiply (bit 8j of a -> 24+j,
+// bit 8j+4 of b<<4 -> 28+j).
+__device__ __forceinline__ uint32_t pack8_01(uint32_t a, uint32_t b) {
+    return ((a | (b << 4)) * 0x01020408u) >> 24;
+}
+__device__ __forceinline__ uint32_t pack16_01(uint4 v) {
+    return pack8_01(v.x, v.y) | (pack8_01(v.z, v.w) << 8);
+}
 
 // Threshold on load (the paper's im2bw step,
 // PAPER.md:1084-1089): foreground <=> byte > thr.  Bit 7 of every byte of the
@@ -429,8 +438,17 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             v[2 * i + 1] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W + 16));
         }
         if (!THR) {
+            // warp-uniform fast path when every byte the warp loaded is 0 or 1
+            uint32_t o = 0;
 #pragma unroll
-            for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+            for (int j = 0; j < 2 * S; j++) o |= v[j].x | v[j].y | v[j].z | v[j].w;
+            if (!__any_sync(FULL, (o & 0xFEFEFEFEu) != 0u)) {
+#pragma unroll
+                for (int i = 0; i < S; i++) xs[i] = pack16_01(v[2 * i]) | (pack16_01(v[2 * i + 1]) << 16);
+            } else {
+#pragma unroll
+                for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+            }
         } else {
             const uint32_t t4 = (uint32_t)g.thr * 0x01010101u;
 #pragma unroll

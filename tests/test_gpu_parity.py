@@ -102,6 +102,21 @@ def test_nonbinary_bytes_aligned():
     assert_same(img, "bytes16")
 
 
+def test_binary_fast_path_mixed_warps():
+    """K1 packs a warp's pixels with a cheaper gather when every byte it loaded
+    is 0 or 1: a 0/1 image with sparse other non-zero values (2..255, and
+    bytes whose only set bit is not bit 0) puts fast-path and general-path
+    warps side by side, in the same tile and across tiles."""
+    rng = np.random.default_rng(11)
+    img = synth.scaled("c4_voronoi_21600", 640, 4096).copy()
+    m = rng.random(img.shape) < 0.002
+    img[m] = rng.choice(np.array([2, 4, 16, 128, 255, 254], np.uint8), size=int(m.sum()))
+    assert_same(img, "mixed 0/1 and other bytes")
+    img2 = synth.scaled("c3_percolation_8192", 640, 4096).copy()
+    img2[::97, ::61] = 2  # 2 has bit 0 clear: a wrong fast path would drop it
+    assert_same(img2, "sparse 2s")
+
+
 def _mosaic(h, w, gap, off_r, off_c, cols):
     """Every h x w binary pattern once, separated by `gap` background pixels and
     shifted by (off_r, off_c) so patterns straddle tile edges."""
