@@ -1000,7 +1000,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
 // border nodes):  offset(segment) + rank in segment + 1, where the rank of a
 // root among the roots of its segment is its component index minus the
 // components of earlier rows minus the non-root border components before it.
-constexpr int KL_WARPS = 8;
+constexpr int KL_WARPS = 2;  // small CTAs: finer scheduling of the 1-2 waves (measured vs 4, 8, 16)
 struct KLSmem {
     uint32_t nrbits[KL_WARPS][CAPC / 32];  // non-root border components of the warp's tile
     uint16_t wpre[KL_WARPS][CAPC / 32];    // exclusive popcount prefix of nrbits
@@ -1122,12 +1122,13 @@ k_label(Geometry g, Workspace ws) {
 // root of this image's forest, or -- row bands -- a root owned by another
 // band, whose global label arrived in xlab; labels stored here are band-local,
 // K5 adds the band offset).  One warp per tile, over its border nodes.
-__global__ void __launch_bounds__(256)
+constexpr int K4_WARPS = 8;
+__global__ void __launch_bounds__(K4_WARPS * 32)
 k_fixup(Geometry g, Workspace ws) {
     pdl_trigger();
     pdl_wait();
     const int lane = lane_id();
-    const int tile = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int tile = blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     if (tile >= g.nT) return;
     const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
     const int nodebase = tile * g.capb;
@@ -1466,7 +1467,7 @@ cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *lab
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_FIXUP);
-    cudaError_t e = launch_pdl(k_fixup, (g.nT + 7) / 8, 256, 0, stream, g, ws);
+    cudaError_t e = launch_pdl(k_fixup, (g.nT + K4_WARPS - 1) / K4_WARPS, K4_WARPS * 32, 0, stream, g, ws);
     if (e != cudaSuccess) return e;
     mark(K_WRITE);
     e = launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0,
