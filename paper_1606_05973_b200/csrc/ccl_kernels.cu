@@ -749,16 +749,17 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
 // runs of the last row above and the first row below are united along the
 // same two edge families as the strip merge.  Vertical tile edges (incl.
 // corner pixels): one thread per (tile column boundary, row).
-__global__ void __launch_bounds__(256)
+constexpr int K2_WARPS = 4;  // measured vs 2 and 8 warps per CTA
+__global__ void __launch_bounds__(K2_WARPS * 32)
 k_border(Geometry g, Workspace ws, int nh_warps) {
     pdl_trigger();
     pdl_wait();
-    __shared__ uint32_t shd[8][2][WPR], sbs[8][2][WPR];
+    __shared__ uint32_t shd[K2_WARPS][2][WPR], sbs[K2_WARPS][2][WPR];
     constexpr int PCAP = 128;
-    __shared__ uint32_t plist[8][PCAP];  // the edge's unions: (upper run, lower run) ordinals
-    __shared__ int pcnt[8];
+    __shared__ uint32_t plist[K2_WARPS][PCAP];  // the edge's unions: (upper run, lower run) ordinals
+    __shared__ int pcnt[K2_WARPS];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
-    const int gw = blockIdx.x * 8 + wib;
+    const int gw = blockIdx.x * K2_WARPS + wib;
     if (gw < nh_warps) {
         const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
         if (ty % g.tpi == 0) return;  // first tile row of an image of a batch: no edge
@@ -1445,7 +1446,8 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
     const int64_t warps = nh + (nv + 31) / 32;
-    if (warps > 0) e = launch_pdl(k_border, (unsigned)((warps + 7) / 8), 256, 0, stream, g, ws, nh);
+    if (warps > 0)
+        e = launch_pdl(k_border, (unsigned)((warps + K2_WARPS - 1) / K2_WARPS), K2_WARPS * 32, 0, stream, g, ws, nh);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
