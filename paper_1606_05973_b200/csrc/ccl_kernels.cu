@@ -1162,8 +1162,8 @@ k_fixup(Geometry g, Workspace ws) {
 // Labeling phase: one warp per 1024-px row segment.  Lane
 // j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
 // warp is one contiguous 512-byte stretch of the output row.
-constexpr int K5_WARPS = 8;
-__global__ void __launch_bounds__(K5_WARPS * 32, 8)
+constexpr int K5_WARPS = 16;  // measured vs 4 and 8
+__global__ void __launch_bounds__(K5_WARPS * 32, 4)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     pdl_trigger();
     pdl_wait();
