@@ -542,7 +542,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         const uint32_t S_ = s | (cin ? lead : 0u);
         uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
         uint32_t mc = upper_merge_heads(hu, u, up, x, xp, S_);
-        if (rl >= 2) mc &= ~hole_bridged(u, up, sm.bm[rl - 2][lane]);
+        // (K2 also drops the edges whose gap pixel is a hole bridged from the
+        // row above -- redundant ones; here the merges are shared out over the
+        // CTA and cost less than the filter: every listed edge is a real
+        // 8-adjacency of the two runs)
         const int lbase = kidx(rl, sm.hbase[rl][lane]) - 1;
         // the row's merges go to a tile-wide list that all threads work
         // through in P2b (balanced); what does not fit stays in mc
