@@ -872,41 +872,6 @@ struct KNSmem {
     int32_t part, excl;
 };
 
-// Marks the tile's border components that are not roots in nrbits (and counts
-// them per row in nrrow); one warp.
-__device__ __forceinline__ void kn_nonroots(const Workspace &ws, int nodebase, int nborder,
-                                            uint32_t *bits, int nbw, int32_t *nrrow, bool setbits) {
-    const int lane = lane_id();
-    // the parents and (row, component) of 4 nodes per lane are loaded at once
-    int par[4], gcv[4];
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-        const int j = lane + 32 * t;
-        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
-        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
-    }
-    for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
-    nrrow[lane] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-        if (par[t] != nodebase + lane + 32 * t) {
-            const int c = gcv[t] & 0xFFFF;
-            if (setbits) atomicOr(bits + (c >> 5), 1u << (c & 31));
-            atomicAdd(nrrow + (gcv[t] >> 16), 1);
-        }
-    }
-    for (int j = lane + 128; j < nborder; j += 32) {
-        const int node = nodebase + j;
-        if (__ldcg(ws.gparent + node) != node) {
-            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
-            if (setbits) atomicOr(bits + (c >> 5), 1u << (c & 31));
-            atomicAdd(nrrow + (gc >> 16), 1);
-        }
-    }
-    __syncwarp();
-}
-
 __global__ void __launch_bounds__(KN_WARPS * 32, 6)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
     pdl_trigger();
@@ -922,11 +887,34 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
         const int tile = ty * g.nTx + tx;
         const int32_t *meta = ws.meta + (int64_t)tile * META;
+        const int nodebase = tile * g.capb;
+        // every load of the tile at once: the node entries of the first 4*32
+        // node slots do not wait for the node count (they lie inside the
+        // tile's capb slots either way)
         const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
-        kn_nonroots(ws, tile * g.capb, nborder, nullptr, 0, sm.nrrow[w], false);
         const int rf = __ldcg(meta + META_ROWFIRST + lane);
-        const int rfn = lane + 1 < rows ? __ldcg(meta + META_ROWFIRST + lane + 1) : ncomp;
-        if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = rfn - rf - sm.nrrow[w][lane];
+        const int rfx = __ldcg(meta + META_ROWFIRST + (lane + 1 < TH ? lane + 1 : TH));
+        int par[4], gcv[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const int j = lane + 32 * t;
+            par[t] = j < g.capb ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
+            gcv[t] = j < g.capb ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+        }
+        int32_t *nrrow = sm.nrrow[w];
+        nrrow[lane] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 4; t++)
+            if (lane + 32 * t < nborder && par[t] != nodebase + lane + 32 * t) atomicAdd(nrrow + (gcv[t] >> 16), 1);
+        for (int j = lane + 128; j < nborder; j += 32) {
+            const int node = nodebase + j;
+            if (__ldcg(ws.gparent + node) != node) atomicAdd(nrrow + (__ldcg(ws.gnodecomp + node) >> 16), 1);
+        }
+        __syncwarp();
+        const int rfn = lane + 1 < rows ? rfx : ncomp;
+        if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = rfn - rf - nrrow[lane];
+        __syncwarp();
     }
     __syncthreads();
     // ---- phase 2: exclusive scan of the tile row's rows*nTx segment counts
