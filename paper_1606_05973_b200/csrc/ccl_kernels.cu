@@ -1029,14 +1029,14 @@ k_label(Geometry g, Workspace ws) {
     constexpr int KL_NODES = 4;
     int par[KL_NODES], gcv[KL_NODES];
 #pragma unroll
-    for (int t = 0; t < KL_NODES; t++) {
+    for (int t = 0; t < KL_NODES; t++) {  // inside the tile's capb slots: no wait for nborder
         const int j = lane + 32 * t;
-        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : 0;
-        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+        par[t] = j < g.capb ? __ldcg(ws.gparent + nodebase + j) : 0;
+        gcv[t] = j < g.capb ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
     }
     uint32_t rr[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) rr[u] = lane + 32 * u < ncomp ? __ldcg(comprow + lane + 32 * u) : 0u;
+    for (int u = 0; u < 4; u++) rr[u] = lane + 32 * u < g.capc ? __ldcg(comprow + lane + 32 * u) : 0u;
     // non-root border components (bits) and their count per row
     for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
     nrrow[lane] = 0;
