@@ -506,7 +506,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         sm.hbase[rl][lane] = (uint16_t)base;
         if (lane == 0) sm.nrun[rl] = (int)nr;
 #pragma unroll 1
-        for (int o = lane; o < (int)nr; o += 32) vp[kidx(rl, o)] = (uint16_t)kidx(rl, o);
+        for (int o = 2 * lane; o < (int)nr; o += 64) {  // two runs per 32-bit store
+            const uint32_t k = (uint32_t)kidx(rl, o);
+            reinterpret_cast<volatile uint32_t *>(vp)[k >> 1] = k | ((k + 1) << 16);
+        }
     }
     __syncthreads();
     if (stop <= 0) return;
