@@ -36,7 +36,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
 }
 
 enum {
-    A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_COMPROW, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
+    A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
     A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_COUNT
 };
 
@@ -47,7 +47,6 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         H * g.nTx * g.maxrun * 2,       // runcomp
         nT * g.capc * 4,                // compnode
         nT * g.capc * 4,                // complab
-        nT * g.capc,                    // comprow
         nT * g.capb * 4,                // gparent
         nT * g.capb * 8,                // gkey
         nT * g.capb * 4,                // gnodecomp
@@ -93,7 +92,6 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.segoff = reinterpret_cast<int32_t *>(b + offs[A_SEGOFF]);
     w.scanstate = reinterpret_cast<unsigned long long *>(b + offs[A_SCANSTATE]);
     w.ticket = reinterpret_cast<int32_t *>(b + offs[A_TICKET]);
-    w.comprow = reinterpret_cast<uint8_t *>(b + offs[A_COMPROW]);
     w.rowexcl = reinterpret_cast<int32_t *>(b + offs[A_ROWEXCL]);
     w.xlab = nullptr;
     w.boff = nullptr;

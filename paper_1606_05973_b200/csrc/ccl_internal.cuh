@@ -47,7 +47,6 @@ struct Workspace {
     uint16_t *runcomp;    // [H][nTx][maxrun]  tile component of each run of each tile row
     int32_t *compnode;    // [nT][capc]        border-node id of a border component (others unset)
     int32_t *complab;     // [nT][capc]        band-local label of the component (1..N_band)
-    uint8_t *comprow;     // [nT][capc]        tile row of the component's root run
     int32_t *gparent;     // [nT][capb]        global union-find over border components
     int64_t *gkey;        // [nT][capb]        (image row, tile column, run ordinal) key: raster order
     int32_t *gnodecomp;   // [nT][capb]        (root row in tile << 16) | tile component of the node

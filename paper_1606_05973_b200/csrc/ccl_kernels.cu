@@ -678,7 +678,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     const int bfirst = (int)warp_excl_scan((uint32_t)sm.bcnt[lane], btot);
     const int ncomp = (int)rtot, nborder = (int)btot;
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
-    uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
@@ -696,7 +695,6 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             const int c = __shfl_sync(FULL, rowfirst, r / MAXRUN) + (int)(pr & 0x1FFu);
             if (o < n) {
                 dst[o] = (uint16_t)c;
-                if (pk & 0x8000u) comprow[c] = (uint8_t)rl;
             }
             if (hasb) {
                 // node number of the chunk's first border root, for P4c
@@ -1001,6 +999,7 @@ struct KLSmem {
     uint16_t wpre[KL_WARPS][CAPC / 32];    // exclusive popcount prefix of nrbits
     int32_t nrrow[KL_WARPS][TH];           // non-roots per row
     int32_t rbase[KL_WARPS][TH];           // label of the row's first root minus its index
+    int32_t rfirst[KL_WARPS][TH];          // first component of each row
 };
 
 __global__ void __launch_bounds__(KL_WARPS * 32)
@@ -1025,7 +1024,6 @@ k_label(Geometry g, Workspace ws) {
     int32_t *nrrow = sm.nrrow[w];
     const int nodebase = tile * g.capb;
     int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-    const uint8_t *comprow = ws.comprow + (int64_t)tile * g.capc;
     // every independent load of the tile at once: the parent and (row,
     // component) of up to KL_NODES border nodes per lane and the root rows
     // of the first 4*32 components
@@ -1037,9 +1035,6 @@ k_label(Geometry g, Workspace ws) {
         par[t] = j < g.capb ? __ldcg(ws.gparent + nodebase + j) : 0;
         gcv[t] = j < g.capb ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
     }
-    uint32_t rr[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) rr[u] = lane + 32 * u < g.capc ? __ldcg(comprow + lane + 32 * u) : 0u;
     // non-root border components (bits) and their count per row
     for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
     nrrow[lane] = 0;
@@ -1081,19 +1076,30 @@ k_label(Geometry g, Workspace ws) {
     auto nonroots_before = [&](int c) -> int {
         return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
     };
-    // four components per lane in flight, the next four loading meanwhile
-    for (int c0 = lane; c0 < ncomp; c0 += 128) {
-        uint32_t rn[4];
+    {
+        // the root row of component c: the last row whose first component is
+        // <= c (binary search over the tile's row offsets in shared memory)
+        int32_t *fs = sm.rfirst[w];
+        fs[lane] = lane < rows ? f : 0x7FFFFFFF;
+        __syncwarp();
+        for (int c0 = lane; c0 < ncomp; c0 += 128) {
+            int rr4[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) rn[u] = c0 + 128 + 32 * u < ncomp ? __ldcg(comprow + c0 + 128 + 32 * u) : 0u;
+            for (int u = 0; u < 4; u++) {
+                const int c = c0 + 32 * u;
+                int lo = 0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int c = c0 + 32 * u;
-            if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
-            st_keep(complab + c, rb[rr[u]] + c - nonroots_before(c));
+                for (int step = 16; step > 0; step >>= 1)
+                    if (fs[lo + step] <= c) lo += step;
+                rr4[u] = lo;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int c = c0 + 32 * u;
+                if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
+                st_keep(complab + c, rb[rr4[u]] + c - nonroots_before(c));
+            }
         }
-#pragma unroll
-        for (int u = 0; u < 4; u++) rr[u] = rn[u];
     }
     // labels of the root nodes
 #pragma unroll
