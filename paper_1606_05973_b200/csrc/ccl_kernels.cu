@@ -1078,19 +1078,17 @@ k_label(Geometry g, Workspace ws) {
     };
     {
         // the root row of component c: the last row whose first component is
-        // <= c (binary search over the tile's row offsets in shared memory)
+        // <= c (the tile's row offsets in shared memory)
         int32_t *fs = sm.rfirst[w];
         fs[lane] = lane < rows ? f : 0x7FFFFFFF;
         __syncwarp();
+        int lo = 0;  // a lane's components only grow: walk forward (~1.5 rows per 32 components)
         for (int c0 = lane; c0 < ncomp; c0 += 128) {
             int rr4[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int c = c0 + 32 * u;
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1)
-                    if (fs[lo + step] <= c) lo += step;
+                while (lo + 1 < TH && fs[lo + 1] <= c) lo++;
                 rr4[u] = lo;
             }
 #pragma unroll
