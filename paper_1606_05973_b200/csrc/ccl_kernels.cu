@@ -999,7 +999,6 @@ struct KLSmem {
     uint16_t wpre[KL_WARPS][CAPC / 32];    // exclusive popcount prefix of nrbits
     int32_t nrrow[KL_WARPS][TH];           // non-roots per row
     int32_t rbase[KL_WARPS][TH];           // label of the row's first root minus its index
-    int32_t rfirst[KL_WARPS][TH];          // first component of each row
 };
 
 __global__ void __launch_bounds__(KL_WARPS * 32)
@@ -1079,17 +1078,25 @@ k_label(Geometry g, Workspace ws) {
     {
         // the root row of component c: the last row whose first component is
         // <= c (the tile's row offsets in shared memory)
-        int32_t *fs = sm.rfirst[w];
-        fs[lane] = lane < rows ? f : 0x7FFFFFFF;
-        __syncwarp();
-        int lo = 0;  // a lane's components only grow: walk forward (~1.5 rows per 32 components)
-        for (int c0 = lane; c0 < ncomp; c0 += 128) {
+        // Each group of 32 consecutive components (one per lane) sees the
+        // few rows that start inside it through a warp-uniform walk over the
+        // row offsets held by the lanes (lane r = row r): no divergence, no
+        // memory.  rcur = last row starting at or before the group.
+        int rcur = 0;
+        for (int gb = 0; gb < ncomp; gb += 128) {  // warp-uniform trip count (shuffles inside)
+            const int c0 = gb + lane;
             int rr4[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                const int c = c0 + 32 * u;
-                while (lo + 1 < TH && fs[lo + 1] <= c) lo++;
-                rr4[u] = lo;
+                const int base = gb + 32 * u;
+                int myrow = rcur;
+                for (int nr = rcur + 1; nr < rows; nr++) {
+                    const int fnr = __shfl_sync(FULL, f, nr);
+                    if (fnr > base + 31) break;
+                    if (base + lane >= fnr) myrow = nr;
+                    rcur = nr;  // starts before the next group's base
+                }
+                rr4[u] = myrow;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
