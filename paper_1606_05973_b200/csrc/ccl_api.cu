@@ -37,7 +37,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
 
 enum {
     A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
-    A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_COUNT
+    A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_COUNT
 };
 
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
@@ -51,6 +51,7 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         nT * g.capb * 8,                // gkey
         nT * g.capb * 4,                // gnodecomp
         nT * g.capb * 4,                // gnodelab
+        nT * 2 * WPR * 4,               // edgerow
         nT * g.maxrun * 4,              // topnode
         nT * g.maxrun * 4,              // botnode
         (size_t)g.nTx * H * 4,          // leftnode
@@ -83,6 +84,7 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.gkey = reinterpret_cast<int64_t *>(b + offs[A_GKEY]);
     w.gnodecomp = reinterpret_cast<int32_t *>(b + offs[A_GNODECOMP]);
     w.gnodelab = reinterpret_cast<int32_t *>(b + offs[A_GNODELAB]);
+    w.edgerow = reinterpret_cast<uint32_t *>(b + offs[A_EDGEROW]);
     w.topnode = reinterpret_cast<int32_t *>(b + offs[A_TOP]);
     w.botnode = reinterpret_cast<int32_t *>(b + offs[A_BOT]);
     w.leftnode = reinterpret_cast<int32_t *>(b + offs[A_LEFT]);

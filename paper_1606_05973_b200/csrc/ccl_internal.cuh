@@ -51,6 +51,7 @@ struct Workspace {
     int64_t *gkey;        // [nT][capb]        (image row, tile column, run ordinal) key: raster order
     int32_t *gnodecomp;   // [nT][capb]        (root row in tile << 16) | tile component of the node
     int32_t *gnodelab;    // [nT][capb]        band-local label of a root node
+    uint32_t *edgerow;    // [nT][2][WPR]      run masks of the tile's first and last row (for K2)
     int32_t *topnode;     // [nT][maxrun]      node of each run of the tile's first row
     int32_t *botnode;     // [nT][maxrun]      node of each run of the tile's last row
     int32_t *leftnode;    // [nTx][H]          node of the pixel in the tile's first column

@@ -371,17 +371,6 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
     return hu & x1 & (s2 | u2);
 }
 
-// A merge candidate at upper head h is also redundant when the gap before
-// h is a single pixel (upper pixel h-2 is foreground) and the row above the
-// upper row has a foreground pixel at h-1: both upper runs touch that pixel,
-// so the lower run is joined to h's run through edges that are processed
-// anyway (the row pair above, and the edge at h-2 to the left).  Candidates
-// bridged this way are the bulk of them on images with isolated holes.
-__device__ __forceinline__ uint32_t hole_bridged(uint32_t u, uint32_t up, uint32_t d) {
-    const uint32_t dpr = __shfl_up_sync(FULL, d, 1);
-    const uint32_t dp = lane_id() == 0 ? 0u : dpr;
-    return ((u << 2) | (up >> 30)) & ((d << 1) | (dp >> 31));
-}
 
 // THR: foreground <=> byte > g.thr (threshold on load) instead of byte != 0;
 // a separate instantiation so the plain path carries no threshold code.
@@ -736,6 +725,9 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? node_of(kidx(r, sm.nrun[r] - 1)) : -1;
         }
     }
+    // the first and last row's run masks for K2's horizontal edges
+    if (w == NW - 1) ws.edgerow[(int64_t)tile * 2 * WPR + lane] = sm.bm[0][lane];
+    if (w == NW - 2) ws.edgerow[((int64_t)tile * 2 + 1) * WPR + lane] = sm.bm[rows - 1][lane];
     int32_t *meta = ws.meta + (int64_t)tile * META;
     if (w == 0) {  // first component of every tile row (components are in key order)
         meta[META_ROWFIRST + lane] = rowfirst;
@@ -767,10 +759,9 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     if (gw < nh_warps) {
         const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
         if (ty % g.tpi == 0) return;  // first tile row of an image of a batch: no edge
-        const int rx = tile_r0(g, ty), ru = rx - 1;
-        const int gword = tx * WPR + lane;
-        const uint32_t u = run_mask(g, ws.bm, ru, gword, nullptr);
-        const uint32_t x = run_mask(g, ws.bm, rx, gword, nullptr);
+        // the run masks of the two rows, as K1 left them
+        const uint32_t u = __ldcg(ws.edgerow + ((int64_t)((ty - 1) * g.nTx + tx) * 2 + 1) * WPR + lane);
+        const uint32_t x = __ldcg(ws.edgerow + (int64_t)(ty * g.nTx + tx) * 2 * WPR + lane);
         RowView U = make_row(u), X = make_row(x);
         shd[wib][0][lane] = U.hx; sbs[wib][0][lane] = U.base;
         shd[wib][1][lane] = X.hx; sbs[wib][1][lane] = X.base;
@@ -796,14 +787,14 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             add(run_ord(shd[wib][0][lq], sbs[wib][0][lq], q & 31), run_ord(X.hx, X.base, b));
         }
         // upper runs whose leftmost lower neighbour has another leftmost upper
-        // neighbour (see upper_merge_heads / hole_bridged in K1)
+        // neighbour (see upper_merge_heads in K1)
         {
             const uint32_t t = x & dilate(U);
             const uint32_t s = smear_up(t, x);
             const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
             const uint32_t S_ = s | (cin ? (x & ~(x + 1)) : 0u);
-            const uint32_t d = run_mask(g, ws.bm, ru - 1, gword, nullptr);
-            m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_) & ~hole_bridged(u, U.xp, d);
+            // (no hole-bridged filter: it only drops redundant edges)
+            m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_);
         }
         while (m) {
             int b = __ffs(m) - 1;
