@@ -376,6 +376,14 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
 // a separate instantiation so the plain path carries no threshold code.
 // BATCH: a stack of images (tile rows are placed per image); the single-image
 // instantiation keeps the plain row arithmetic.
+// Development knob (scripts/k1_phases.py): K1 truncated after a phase.  Only
+// in builds with -DCCL_PHASE_KNOB=1 -- the checks cost the product K1 ~3 us.
+#if CCL_PHASE_KNOB
+#define K1_STOP(cond) \
+    if (cond) return
+#else
+#define K1_STOP(cond) (void)0
+#endif
 template <bool THR, bool BATCH>
 __global__ void __launch_bounds__(NW * 32, 5)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
@@ -469,7 +477,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     if (lane < S) sm.bcnt[r0 + lane] = 0;
     if (threadIdx.x == 0) sm.nmerge = 0;
     __syncthreads();
-    if (stop < 0) return;
+    K1_STOP(stop < 0);
     // ---- P0b: run mask = foreground + bridged single-pixel holes (a background
     // pixel whose left and right neighbours and the pixel above or below are
     // foreground).  Only holes whose neighbours lie in
@@ -501,7 +509,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         }
     }
     __syncthreads();
-    if (stop <= 0) return;
+    K1_STOP(stop <= 0);
 
     // ---- P2a: scan.  A run with a foreground pixel among the three above any
     // of its pixels copies its leftmost upper neighbour's label (the decision
@@ -568,7 +576,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         __syncwarp();
     }
     __syncthreads();
-    if (stop <= 1) return;
+    K1_STOP(stop <= 1);
     // ---- P2b: the remaining edges, merged with lock-free Rem's splicing
     // (the decision tree's copy(c,a)/copy(c,d) merges).  The
     // parent chains may still cross strips (a strip's first row points into
@@ -605,7 +613,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         }
     }
     __syncthreads();
-    if (stop <= 2) return;
+    K1_STOP(stop <= 2);
     // ---- P3: flatten -- every run -> its root (Alg. flatten's p[i] <- p[p[i]],
     // PAPER.md:711-712), own rows, lane = run ordinal.  A root r's entry
     // becomes 0x8000 | (its rank among the roots of its row); finds treat a
@@ -655,7 +663,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         if (lane == 0) sm.rowcnt[rl] = cnt;
     }
     __syncthreads();
-    if (stop <= 3) return;
+    K1_STOP(stop <= 3);
     // ---- P4: roots in index order = raster order of first pixels get the
     // consecutive component numbers (Alg. flatten's k++):
     // component = (roots in earlier rows) + (rank in its row).  Every run ->
@@ -703,7 +711,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         }
     }
     __syncthreads();
-    if (stop <= 4) return;
+    K1_STOP(stop <= 4);
     // ---- P4c: nodes of the border pixels (for K2).  A border run's root r is
     // a border root; its node is the chunk's first node number (P4) plus the
     // border roots before it in its bitmap word -- all in shared memory.

@@ -1,6 +1,7 @@
 """K1 truncated after each phase (ccl_debug_set(1, stop)), one launch per
 stop -- run under ncu --metrics smsp__inst_executed.sum to get the
-instruction count of every phase (cumulative)."""
+instruction count of every phase (cumulative).  Needs the knob build (see
+scripts/k1_phases.py)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth

@@ -1,5 +1,7 @@
 """Development timing of K1's phases: K1 truncated after phase `stop` (the
-rest of the pipeline is skipped), CUDA events per kernel."""
+rest of the pipeline is skipped), CUDA events per kernel.  Needs the knob
+build:  CCL_VARIANT=knob CCL_DEFS=-DCCL_PHASE_KNOB=1 python build_native.py product
+and  CCL_B200_LIB=libccl_knob.so python scripts/k1_phases.py"""
 import sys, os, ctypes
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
 import torch, synth
