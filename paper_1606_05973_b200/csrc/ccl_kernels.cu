@@ -584,13 +584,15 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // The tile's merge list is shared out over all 256 threads (a strip with
     // many merges no longer holds the barrier); rows whose merges did not fit
     // in the list finish them per lane below.
-    {
-        const int nm = min(sm.nmerge, MLCAP);
-        for (int i = threadIdx.x; i < nm; i += NW * 32) {
-            const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
-            if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
-        }
+    const int nmerge = sm.nmerge;
+    for (int i = threadIdx.x; i < min(nmerge, MLCAP); i += NW * 32) {
+        const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
+        if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
     }
+    if (nmerge <= MLCAP) {  // nothing left per lane: clear the rows for bbits
+#pragma unroll
+        for (int i = 0; i < S; i++) sm.mc[r0 + i][lane] = 0u;
+    } else
 #pragma unroll 1
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
