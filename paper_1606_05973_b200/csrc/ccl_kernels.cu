@@ -49,10 +49,14 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Component labels (K3b/K4) are stored with the evict_last L2 priority: K5
-// gathers them while 1.87 GB of evict_first label stores stream past (-4 us).
-__device__ __forceinline__ void st_keep(int32_t *p, int32_t v) {
+// gathers them while 1.87 GB of evict_first label stores stream past (-4 us);
+// the policy is made once per thread.
+__device__ __forceinline__ uint64_t pol_evict_last() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_keep(int32_t *p, int32_t v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
 }
 
@@ -1024,6 +1028,7 @@ k_label(Geometry g, Workspace ws) {
     int32_t *nrrow = sm.nrrow[w];
     const int nodebase = tile * g.capb;
     int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+    const uint64_t keep = pol_evict_last();  // component labels stay in L2 for K5
     // every independent load of the tile at once: the parent and (row,
     // component) of up to KL_NODES border nodes per lane and the root rows
     // of the first 4*32 components
@@ -1103,7 +1108,7 @@ k_label(Geometry g, Workspace ws) {
             for (int u = 0; u < 4; u++) {
                 const int c = c0 + 32 * u;
                 if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
-                st_keep(complab + c, rb[rr4[u]] + c - nonroots_before(c));
+                st_keep(complab + c, rb[rr4[u]] + c - nonroots_before(c), keep);
             }
         }
     }
@@ -1140,6 +1145,7 @@ k_fixup(Geometry g, Workspace ws) {
     const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
     const int nodebase = tile * g.capb;
     int32_t *complab = ws.complab + (int64_t)tile * g.capc;
+    const uint64_t keep = pol_evict_last();  // component labels stay in L2 for K5
     // the parents and components of 4 nodes per lane are loaded at once
     int par[4], gcv[4];
 #pragma unroll
@@ -1153,14 +1159,14 @@ k_fixup(Geometry g, Workspace ws) {
         if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
         const int r = par[t] < 0 ? par[t] : gfind_ro(ws.gparent, par[t]);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(complab + (gcv[t] & 0xFFFF), lab);
+        st_keep(complab + (gcv[t] & 0xFFFF), lab, keep);
     }
     for (int j = lane + 128; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) == node) continue;
         const int r = gfind_ro(ws.gparent, node);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(complab + (__ldcg(ws.gnodecomp + node) & 0xFFFF), lab);
+        st_keep(complab + (__ldcg(ws.gnodecomp + node) & 0xFFFF), lab, keep);
     }
 }
 
