@@ -642,14 +642,11 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
                 // copied the same upper-strip run, so it is compressed too
                 const uint32_t j = vp[k];
                 uint32_t r = j;
-                if (!(j & 0x8000u)) {
-                    while (true) {
-                        const uint32_t v = vp[r];
-                        if (v == r || (v & 0x8000u)) break;
-                        r = v;
-                    }
-                } else {
-                    r = (uint32_t)k;  // unreachable: nobody flags another warp's runs
+                // (j is never flagged: only this warp ranks its own runs, below)
+                while (true) {
+                    const uint32_t v = vp[r];
+                    if (v == r || (v & 0x8000u)) break;
+                    r = v;
                 }
                 root = r == (uint32_t)k;
                 if (!root) {
