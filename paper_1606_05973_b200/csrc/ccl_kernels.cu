@@ -406,10 +406,10 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     volatile uint16_t *vp = sm.p;
     uint32_t *bbits = &sm.mc[0][0];
 
-    // Warm L2 with the pixels of the tile that will start about half a wave
-    // of resident CTAs later (pfd = half the resident CTAs on the device;
-    // measured against 1x, 1.5x and 2x): its loads then hit L2 instead of
-    // waiting on HBM.
+    // Warm L2 with the pixels of the tile that will start about a quarter
+    // wave of resident CTAs later (pfd = a quarter of the resident CTAs on
+    // the device; measured against 3/8, 1/2, 5/8, 1, 1.5 and 2 waves): its
+    // loads then hit L2 instead of waiting on HBM.
     {
         const int pt = blockIdx.x + pfd;
         if (pfd > 0 && pt < g.nT) {
@@ -1447,7 +1447,7 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     const bool batch = g.tpi != g.nTy;
     auto k1 = g.thr ? (batch ? k_tile_local<true, true> : k_tile_local<true, false>)
                     : (batch ? k_tile_local<false, true> : k_tile_local<false, false>);
-    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_exper ? 0 : g_k1_resident / 2,
+    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_exper ? 0 : g_k1_resident / 4,
                    g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
