@@ -1093,10 +1093,13 @@ k_label(Geometry g, Workspace ws) {
             for (int u = 0; u < 4; u++) {
                 const int base = gb + 32 * u;
                 int myrow = rcur;
-                for (int nr = rcur + 1; nr < rows; nr++) {
-                    const int fnr = __shfl_sync(FULL, f, nr);
-                    if (fnr > base + 31) break;
-                    if (base + lane >= fnr) myrow = nr;
+                // the rows after rcur that start inside this group (rows are
+                // sorted by their first component; lane = row)
+                uint32_t starts = __ballot_sync(FULL, lane > rcur && lane < rows && f <= base + 31);
+                while (starts) {
+                    const int nr = __ffs(starts) - 1;
+                    starts &= starts - 1;
+                    if (base + lane >= __shfl_sync(FULL, f, nr)) myrow = nr;
                     rcur = nr;  // starts before the next group's base
                 }
                 rr4[u] = myrow;
