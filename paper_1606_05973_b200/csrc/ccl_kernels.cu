@@ -388,7 +388,7 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
 #else
 #define K1_STOP(cond) (void)0
 #endif
-template <bool THR, bool BATCH>
+template <bool THR, bool BATCH, bool BANDS = false>
 __global__ void __launch_bounds__(NW * 32, 5)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
     pdl_trigger();
@@ -704,7 +704,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
                 const uint32_t bbal = __ballot_sync(FULL, broot);
                 if (broot) {
                     const int node = nodebase + bi + __popc(bbal & ((1u << lane) - 1u));
-                    compnode[c] = node;
+                    if (BANDS) compnode[c] = node;  // only the row-band path reads it
                     ws.gparent[node] = node;
                     ws.gnodecomp[node] = (rl << 16) | c;
                     ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
@@ -1424,7 +1424,7 @@ static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     for (auto k : {k_tile_local<false, false>, k_tile_local<true, false>, k_tile_local<false, true>,
-                   k_tile_local<true, true>})
+                   k_tile_local<true, true>, k_tile_local<false, false, true>, k_tile_local<true, false, true>})
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))) !=
             cudaSuccess)
             return e;
@@ -1447,9 +1447,9 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
         if (ev) cudaEventRecord(ev[i], stream);
     };
     mark(K_TILE);
-    const bool batch = g.tpi != g.nTy;
-    auto k1 = g.thr ? (batch ? k_tile_local<true, true> : k_tile_local<true, false>)
-                    : (batch ? k_tile_local<false, true> : k_tile_local<false, false>);
+    const bool batch = g.tpi != g.nTy, bands = ws.boff != nullptr;  // (a band workspace has its offset)
+    auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
+                    : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
     e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_exper ? 0 : g_k1_resident / 4,
                    g_k1_stop);
     if (e != cudaSuccess) return e;
