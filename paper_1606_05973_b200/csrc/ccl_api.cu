@@ -37,7 +37,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
 
 enum {
     A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
-    A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_COUNT
+    A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_K1OVER, A_COUNT
 };
 
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
@@ -62,6 +62,7 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         (size_t)g.nTy * 8,              // scanstate
         16,                             // ticket
         (size_t)g.nTy * 4,              // rowexcl
+        (nT + 1) * 4,                   // k1over + its count
     };
     size_t o = 0;
     for (int i = 0; i < A_COUNT; i++) {
@@ -95,9 +96,15 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.scanstate = reinterpret_cast<unsigned long long *>(b + offs[A_SCANSTATE]);
     w.ticket = reinterpret_cast<int32_t *>(b + offs[A_TICKET]);
     w.rowexcl = reinterpret_cast<int32_t *>(b + offs[A_ROWEXCL]);
+    w.k1over = reinterpret_cast<int32_t *>(b + offs[A_K1OVER]);
+    w.k1over_n = w.k1over + g.nT;
     w.xlab = nullptr;
     w.boff = nullptr;
     return w;
+}
+
+cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream) {
+    return cudaMemsetAsync(ws.k1over_n, 0, sizeof(int32_t), stream);
 }
 
 }  // namespace cclb
@@ -195,7 +202,8 @@ static ccl_status label_oneshot(const uint8_t *img, int B, int H, int W, int thr
     if (e == cudaErrorMemoryAllocation) return CCL_OUT_OF_MEMORY;
     if (e != cudaSuccess) return CCL_CUDA_ERROR;
     Workspace ws = workspace_bind(g, mem);
-    e = run_pipeline(g, ws, img, labels, n_components, s, nullptr);
+    e = workspace_init(ws, s);
+    if (e == cudaSuccess) e = run_pipeline(g, ws, img, labels, n_components, s, nullptr);
     cudaError_t e2 = cudaFreeAsync(mem, s);
     if (e != cudaSuccess || e2 != cudaSuccess) return CCL_CUDA_ERROR;
     return CCL_OK;
@@ -223,6 +231,11 @@ ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out) {
         return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
     }
     p->ws = workspace_bind(p->g, p->ws_mem);
+    if (workspace_init(p->ws, 0) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaFree(p->ws_mem);
+        delete p;
+        return CCL_CUDA_ERROR;
+    }
     *plan_out = p;
     return CCL_OK;
 }

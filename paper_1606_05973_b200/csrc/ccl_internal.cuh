@@ -62,6 +62,8 @@ struct Workspace {
     unsigned long long *scanstate;  // [nTy]   decoupled-lookback descriptors (one per tile row)
     int32_t *ticket;      // [1]               dynamic partition counter
     int32_t *rowexcl;     // [nTy]             labels of earlier tile rows
+    int32_t *k1over;      // [nT]              tiles K1 handed to its full-size pass
+    int32_t *k1over_n;    // [1]               their count (0 between calls; K3 resets it)
     // row bands only (null for a whole image):
     const int32_t *xlab;  // [nb*2W]           exported labels of all bands' boundary slots; a
                           //                   node whose parent is -2-f takes xlab[f]
@@ -89,6 +91,8 @@ __host__ __device__ __forceinline__ int row_tile(const Geometry &g, int row) {
 // Offsets of every Workspace array inside one allocation of *total bytes.
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
+// Zeroes the counters a new workspace must start with (before its first call).
+cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream);
 
 
 enum { K_TILE = 0, K_BORDER, K_NUMBER, K_LABEL, K_FIXUP, K_WRITE, K_COUNT };

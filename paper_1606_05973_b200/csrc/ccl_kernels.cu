@@ -339,8 +339,13 @@ __device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *
 // first pixel.  Every warp owns S consecutive rows (a strip); per-run work is
 // done a row at a time with lane = run ordinal.
 constexpr int MLCAP = 256;  // P2a -> P2b merge list entries (the rest stay in mc)
-struct K1Smem {
-    uint16_t p[RCAP];              // parent of each run (the union-find array p of Alg. merge)
+// Runs per tile row the main K1 holds in shared memory (16 KB union-find
+// array: 6 CTAs/SM).  A tile with a row of more runs (alternating pixels)
+// is left to k_tile_big, which holds the full MAXRUN per row (5 CTAs/SM).
+constexpr int K1_MR = 256;
+template <int MR>
+struct K1SmemT {
+    uint16_t p[TH * MR];           // parent of each run (the union-find array p of Alg. merge)
     uint32_t bm[TH][WPR];          // run masks (foreground + filled holes)
     // P0: raw foreground; P2a/P2b: upper-side merge heads; P3 on: bitmap of
     // the roots of components that touch the tile border (run k = r*MAXRUN+o
@@ -355,8 +360,7 @@ struct K1Smem {
     uint32_t mlist[MLCAP];         // P2a -> P2b: merge pairs (upper run | lower run << 16)
     int32_t nmerge;
 };
-
-__device__ __forceinline__ int kidx(int r, int o) { return r * MAXRUN + o; }
+using K1Smem = K1SmemT<MAXRUN>;
 
 // Upper-side edges that the copy step does not already cover.  The edge set
 // {(L, leftmost upper run of L)} U {(U, leftmost lower run of U)} connects
@@ -388,16 +392,17 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
 #else
 #define K1_STOP(cond) (void)0
 #endif
-template <bool THR, bool BATCH, bool BANDS = false>
-__global__ void __launch_bounds__(NW * 32, 5)
-k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
-    pdl_trigger();
+// MR: runs per row held in shared memory (K1_MR in k_tile_local, MAXRUN in
+// k_tile_big).  Run (row r, ordinal o) has index k = r*MR + o.
+template <bool THR, bool BATCH, bool BANDS, int MR>
+__device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const Geometry &g, const Workspace &ws,
+                                        const int tile, int pfd, int stop) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    K1Smem &sm = *reinterpret_cast<K1Smem *>(smem_raw);
+    K1SmemT<MR> &sm = *reinterpret_cast<K1SmemT<MR> *>(smem_raw);
+    auto kidx = [](int r, int o) { return r * MR + o; };
 
     const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int tx = blockIdx.x % g.nTx, ty = blockIdx.x / g.nTx;
-    const int tile = blockIdx.x;
+    const int tx = tile % g.nTx, ty = tile / g.nTx;
     const int R0 = BATCH ? tile_r0(g, ty) : ty * TH, C0 = tx * TW;
     const int rows = BATCH ? tile_rows(g, ty) : min(TH, g.H - R0);
     const int vcols = min(TW, g.W - C0);
@@ -411,7 +416,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // the device; measured against 3/8, 1/2, 5/8, 1, 1.5 and 2 waves): its
     // loads then hit L2 instead of waiting on HBM.
     {
-        const int pt = blockIdx.x + pfd;
+        const int pt = tile + pfd;
         if (pfd > 0 && pt < g.nT) {
             const int pty = pt / g.nTx;
             const int prow = (BATCH ? tile_r0(g, pty) : pty * TH) + (threadIdx.x >> 3);
@@ -466,7 +471,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // (K5's label stores are evict_first), measured -10 us on C4
     uint64_t pol_last;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-    if (blockIdx.x == 0) {  // reset the numbering scan's lookback state (K3)
+    if (MR < MAXRUN && tile == 0) {  // reset the numbering scan's lookback state (K3)
         for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
     }
@@ -489,6 +494,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
     // partition of the foreground, and K2/K5 read the same run mask.
     // Then run heads, per-word run counts, and every run starts as its own
     // label.
+    bool over = false;  // a row of this warp has more runs than the p array holds
 #pragma unroll
     for (int i = 0; i < S; i++) {
         const int rl = r0 + i;
@@ -506,13 +512,21 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         sm.bm[rl][lane] = x;
         sm.hbase[rl][lane] = (uint16_t)base;
         if (lane == 0) sm.nrun[rl] = (int)nr;
+        over |= (int)nr > MR;
 #pragma unroll 1
-        for (int o = 2 * lane; o < (int)nr; o += 64) {  // two runs per 32-bit store
+        for (int o = 2 * lane; o < min((int)nr, MR); o += 64) {  // two runs per 32-bit store
             const uint32_t k = (uint32_t)kidx(rl, o);
             reinterpret_cast<volatile uint32_t *>(vp)[k >> 1] = k | ((k + 1) << 16);
         }
     }
-    __syncthreads();
+    if (MR < MAXRUN) {
+        if (__syncthreads_or(over)) {  // too many runs in a row: k_tile_big takes the tile
+            if (threadIdx.x == 0) ws.k1over[atomicAdd(ws.k1over_n, 1)] = tile;
+            return;
+        }
+    } else {
+        __syncthreads();
+    }
     K1_STOP(stop <= 0);
 
     // ---- P2a: scan.  A run with a foreground pixel among the three above any
@@ -655,8 +669,8 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
                 }
                 if (edge_row || (o == 0 && lfirst) || (o == n - 1 && llast)) {
                     const uint32_t bit = 1u << (r & 31);
-                    uint32_t *wd = bbits + (r / MAXRUN) * WPR + ((r % MAXRUN) >> 5);
-                    if (!(atomicOr(wd, bit) & bit)) atomicAdd(&sm.bcnt[r / MAXRUN], 1);
+                    uint32_t *wd = bbits + (r / MR) * WPR + ((r % MR) >> 5);
+                    if (!(atomicOr(wd, bit) & bit)) atomicAdd(&sm.bcnt[r / MR], 1);
                 }
             }
             const uint32_t bal = __ballot_sync(FULL, root);
@@ -692,7 +706,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             const uint32_t pk = o < n ? sm.p[k] : 0u;
             const int r = (pk & 0x8000u) ? k : (int)pk;
             const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
-            const int c = __shfl_sync(FULL, rowfirst, r / MAXRUN) + (int)(pr & 0x1FFu);
+            const int c = __shfl_sync(FULL, rowfirst, r / MR) + (int)(pr & 0x1FFu);
             if (o < n) {
                 dst[o] = (uint16_t)c;
             }
@@ -722,7 +736,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         auto node_of = [&](int k) -> int {
             const uint32_t pk = sm.p[k];
             const int r = (pk & 0x8000u) ? k : (int)pk;
-            const int rr = r / MAXRUN, ro = r % MAXRUN;
+            const int rr = r / MR, ro = r % MR;
             return nodebase + sm.hbase[rr][ro >> 5] + __popc(bbits[rr * WPR + (ro >> 5)] & ((1u << (ro & 31)) - 1u));
         };
         const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
@@ -748,6 +762,27 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
             meta[META_NBORDER] = nborder;
             meta[META_ROWS] = rows;
         }
+    }
+}
+
+template <bool THR, bool BATCH, bool BANDS = false>
+__global__ void __launch_bounds__(NW * 32, 6)
+k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
+    pdl_trigger();
+    k1_tile<THR, BATCH, BANDS, K1_MR>(img, g, ws, blockIdx.x, pfd, stop);
+}
+
+// The tiles k_tile_local handed over (a row with more than K1_MR runs); the
+// list is final once k_tile_local completed.  Usually empty.
+template <bool THR, bool BATCH, bool BANDS = false>
+__global__ void __launch_bounds__(NW * 32, 5)
+k_tile_big(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) {
+    pdl_trigger();
+    pdl_wait();
+    const int n = __ldcg(ws.k1over_n);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        k1_tile<THR, BATCH, BANDS, MAXRUN>(img, g, ws, __ldcg(ws.k1over + i), 0, stop);
+        __syncthreads();  // shared memory is reused by the next tile
     }
 }
 
@@ -879,6 +914,7 @@ __global__ void __launch_bounds__(KN_WARPS * 32, 6)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
     pdl_trigger();
     pdl_wait();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
     __shared__ KNSmem sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
@@ -1399,7 +1435,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);
+    return 6 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3-K5, K2 if any edge
 }
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
@@ -1420,11 +1456,17 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned bl
 }
 
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
+static int g_k1big_resident = 0;
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     for (auto k : {k_tile_local<false, false>, k_tile_local<true, false>, k_tile_local<false, true>,
                    k_tile_local<true, true>, k_tile_local<false, false, true>, k_tile_local<true, false, true>})
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
+            return e;
+    for (auto k : {k_tile_big<false, false>, k_tile_big<true, false>, k_tile_big<false, true>, k_tile_big<true, true>,
+                   k_tile_big<false, false, true>, k_tile_big<true, false, true>})
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))) !=
             cudaSuccess)
             return e;
@@ -1432,9 +1474,13 @@ static cudaError_t set_attrs() {
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false, false>, NW * 32,
-                                                           sizeof(K1Smem))) != cudaSuccess)
+                                                           sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
         return e;
     g_k1_resident = sms * per;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_big<false, false>, NW * 32,
+                                                           sizeof(K1Smem))) != cudaSuccess)
+        return e;
+    g_k1big_resident = sms * per;
     g_attr_done = true;
     return cudaSuccess;
 }
@@ -1450,8 +1496,12 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     const bool batch = g.tpi != g.nTy, bands = ws.boff != nullptr;  // (a band workspace has its offset)
     auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
                     : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
-    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_exper ? 0 : g_k1_resident / 4,
-                   g_k1_stop);
+    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1SmemT<K1_MR>), stream, img, g, ws,
+                   g_k1_exper ? 0 : g_k1_resident / 4, g_k1_stop);
+    if (e != cudaSuccess) return e;
+    auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
+                     : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
+    e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
     if (g_k1_stop < 99) return cudaGetLastError();
