@@ -1501,7 +1501,8 @@ cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_
     if (e != cudaSuccess) return e;
     auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
                      : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
-    e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
+    // a small grid (usually there is nothing to do; its CTAs loop over the list)
+    e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident / 2), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
     if (g_k1_stop < 99) return cudaGetLastError();
