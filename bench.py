@@ -366,10 +366,15 @@ def main():
                     "kernels": kern}
         # K1 moves 1 B/px of algorithmic bytes but is bound by instruction
         # issue (shared-memory union-find, bit-parallel scans): its issue
-        # utilisation is the roofline that binds it
-        iss = ncu_issue(dom, args.workload)
+        # utilisation is the roofline that binds it; every kernel's issue
+        # utilisation goes with its entry
+        for k in kern:
+            iss = ncu_issue(k, args.workload)
+            if iss is not None:
+                kern[k]["issue"] = iss
+        iss = ncu_issue("k_tile_local", args.workload)
         if iss is not None:
-            roofline["issue"] = iss
+            roofline["issue"] = dict(iss, kernel="k_tile_local")
 
     line = {
         "metric": METRIC, "value": value, "unit": "Gpx/s", "n_gpus": ws, "steps": args.steps,
