@@ -338,7 +338,7 @@ __device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *
 // labels, so "link to the smaller index" keeps every root at its component's
 // first pixel.  Every warp owns S consecutive rows (a strip); per-run work is
 // done a row at a time with lane = run ordinal.
-constexpr int MLCAP = 256;  // P2a -> P2b merge list entries (the rest stay in mc)
+constexpr int MLCAP = 256;  // P2a -> P2b merge list entries in k_tile_big (4x in k_tile_local; the rest stay in mc)
 // Runs per tile row the main K1 holds in shared memory (16 KB union-find
 // array: 6 CTAs/SM).  A tile with a row of more runs (alternating pixels)
 // is left to k_tile_big, which holds the full MAXRUN per row (5 CTAs/SM).
@@ -357,7 +357,7 @@ struct K1SmemT {
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t bcnt[TH];              // border components whose root run lies in the row
-    uint32_t mlist[MLCAP];         // P2a -> P2b: merge pairs (upper run | lower run << 16)
+    uint32_t mlist[MR == MAXRUN ? MLCAP : 4 * MLCAP];  // P2a -> P2b: merge pairs (upper | lower << 16)
     int32_t nmerge;
 };
 using K1Smem = K1SmemT<MAXRUN>;
@@ -569,7 +569,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         // through in P2b (balanced); what does not fit stays in mc
         if (mc) {
             int idx = atomicAdd(&sm.nmerge, __popc(mc));
-            while (mc && idx < MLCAP) {
+            while (mc && idx < (MR == MAXRUN ? MLCAP : 4 * MLCAP)) {
                 const int b = __ffs(mc) - 1;
                 const int a = ub + __popc(hu & upto(b)) - 1;         // the upper run with head h
                 const int c = lbase + __popc(hx & ((1u << b) - 1u));  // the lower run containing h-1
@@ -603,11 +603,12 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // many merges no longer holds the barrier); rows whose merges did not fit
     // in the list finish them per lane below.
     const int nmerge = sm.nmerge;
-    for (int i = threadIdx.x; i < min(nmerge, MLCAP); i += NW * 32) {
+    constexpr int MLC = MR == MAXRUN ? MLCAP : 4 * MLCAP;
+    for (int i = threadIdx.x; i < min(nmerge, MLC); i += NW * 32) {
         const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
         if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
     }
-    if (nmerge <= MLCAP) {  // nothing left per lane: clear the rows for bbits
+    if (nmerge <= MLC) {  // nothing left per lane: clear the rows for bbits
 #pragma unroll
         for (int i = 0; i < S; i++) sm.mc[r0 + i][lane] = 0u;
     } else
