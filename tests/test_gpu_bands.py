@@ -76,3 +76,15 @@ def test_nccl_sharded_single_rank():
         assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo)
     plan.close()
     comm.close()
+
+
+@pytest.mark.parametrize("nb", [1, 3])
+def test_bands_with_handed_over_tiles(nb):
+    """Row bands whose tiles go to K1's full-size pass (long rows)."""
+    img = synth.scaled("c3_percolation_8192", 300, 2100).copy()
+    for r in range(10, 299, 37):  # isolated alternating rows: 512 runs per tile row
+        img[r - 1:r + 2] = 0
+        img[r, ::2] = 1
+    lb, nb_ = banded(img, nb)
+    lo, no = oracle.label(img)
+    assert nb_ == no and np.array_equal(lb, lo)

@@ -66,3 +66,23 @@ def test_batch_of_one_equals_single():
     b, nb = ccl.label_batch(torch.from_numpy(img[None]).cuda())
     torch.cuda.synchronize()
     assert int(na.item()) == int(nb[0].item()) and torch.equal(a, b[0])
+
+
+def _long_rows(img, rows):
+    """Isolated alternating rows (the rows around them empty, so the hole fill
+    bridges nothing): 512 runs per 1024-px tile row -- more than the 256 the
+    main K1 holds, so those tiles go to K1's full-size pass."""
+    img = img.copy()
+    for r in rows:
+        img[max(r - 1, 0):r + 2] = 0
+        img[r, ::2] = 1
+    return img
+
+
+def test_batch_with_handed_over_tiles():
+    """Batched images whose tiles mix the main K1 and its hand-over pass."""
+    base = synth.scaled("c4_voronoi_21600", 40, 1100)
+    imgs = np.stack([_long_rows(base, [3, 20, 39]), base, _long_rows(synth.bernoulli(40, 1100, 0.5, seed=9), [0, 33]),
+                     _long_rows(np.zeros((40, 1100), np.uint8), [31, 32])])
+    check_batch(imgs)
+    check_batch(imgs, use_plan=True)

@@ -64,3 +64,15 @@ def test_im2bw_level_half():
     torch.cuda.synchronize()
     lo, no = oracle.label((img >= 128).astype(np.uint8))
     assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo)
+
+
+def test_threshold_handed_over_tiles():
+    """Threshold on load in K1's full-size pass: rows alternating between
+    values just above and just below t (512 runs per tile row)."""
+    H, W = 70, 2100
+    img = gray_image(H, W, 5)
+    for r in range(3, H - 1, 7):  # isolated: the rows around are below t
+        img[r - 1:r + 2] = 100
+        img[r, ::2] = 200
+    for use_plan in (False, True):
+        check(img, 150, use_plan)
