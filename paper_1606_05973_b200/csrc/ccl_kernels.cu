@@ -1143,9 +1143,11 @@ k_label(Geometry g, Workspace ws) {
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                const int c = c0 + 32 * u;
-                if (c >= ncomp || ((bits[c >> 5] >> (c & 31)) & 1u)) continue;  // not a root: K4
-                st_keep(complab + c, rb[rr4[u]] + c - nonroots_before(c), keep);
+                // a group is exactly one word of the non-root bitmap (c = base + lane)
+                const int c = c0 + 32 * u, wi = (gb >> 5) + u;
+                const uint32_t wb = bits[wi];
+                if (c >= ncomp || ((wb >> lane) & 1u)) continue;  // not a root: K4
+                st_keep(complab + c, rb[rr4[u]] + c - (wpre[wi] + __popc(wb & ((1u << lane) - 1u))), keep);
             }
         }
     }
