@@ -1040,14 +1040,11 @@ struct KLSmem {
     int32_t rbase[KL_WARPS][TH];           // label of the row's first root minus its index
 };
 
-__global__ void __launch_bounds__(KL_WARPS * 32)
-k_label(Geometry g, Workspace ws) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ KLSmem sm;
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int tile = blockIdx.x * KL_WARPS + w;
-    if (tile >= g.nT) return;
+#ifndef KL_TPW
+#define KL_TPW 1  // tiles per warp (grid-stride)
+#endif
+__device__ __forceinline__ void label_tile(const Geometry &g, const Workspace &ws, KLSmem &sm, int tile, int w,
+                                           int lane) {
     const int tx = tile % g.nTx, ty = tile / g.nTx;
     const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
     const int32_t *meta = ws.meta + (int64_t)tile * META;
@@ -1165,6 +1162,18 @@ k_label(Geometry g, Workspace ws) {
         if (__ldcg(ws.gparent + node) != node) continue;
         const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
         ws.gnodelab[node] = rb[gc >> 16] + c - nonroots_before(c);
+    }
+}
+
+__global__ void __launch_bounds__(KL_WARPS * 32)
+k_label(Geometry g, Workspace ws) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ KLSmem sm;
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    for (int tile = blockIdx.x * KL_WARPS + w; tile < g.nT; tile += gridDim.x * KL_WARPS) {
+        label_tile(g, ws, sm, tile, w, lane);
+        __syncwarp();  // the warp's shared arrays are reused by its next tile
     }
 }
 
@@ -1524,7 +1533,7 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
     cudaError_t e = launch_pdl(k_number, g.nTy, KN_WARPS * 32, 0, stream, g, ws, n_components);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[K_LABEL], stream);
-    e = launch_pdl(k_label, (g.nT + KL_WARPS - 1) / KL_WARPS, KL_WARPS * 32, 0, stream, g, ws);
+    e = launch_pdl(k_label, (g.nT + KL_WARPS * KL_TPW - 1) / (KL_WARPS * KL_TPW), KL_WARPS * 32, 0, stream, g, ws);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
