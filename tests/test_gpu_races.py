@@ -32,3 +32,35 @@ def test_repeated_runs_bit_exact(name, reps):
         if int(n.item()) != no or not torch.equal(out, ref):
             bad.append(i)
     assert not bad, f"{name}: runs {bad} of {reps} differ from the oracle"
+
+
+@pytest.mark.parametrize("name,h,w", [("c3_percolation_8192", 1024, 2048), ("c4_voronoi_21600", 700, 3000),
+                                      ("c2_blobs_1024", 1024, 1024)])
+def test_plans_on_concurrent_streams(name, h, w):
+    """Frames in flight at once (scripts/pipelined_probe.py): each plan owns its
+    workspace, so two plans on two streams, and one-shot calls on a third,
+    overlap freely; every output is bit-exact with the oracle."""
+    imgs = [synth.scaled(name, h, w), synth.bernoulli(h, w, 0.45, seed=7), synth.scaled(name, h, w)[::-1].copy()]
+    want = [oracle.label(im) for im in imgs]
+    g = [torch.from_numpy(im).cuda() for im in imgs]
+    plans = [ccl.Plan(h, w), ccl.Plan(h, w)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    torch.cuda.synchronize()
+    for k in range(12):
+        i = k % 3
+        s = streams[i]
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            out = torch.empty((h, w), dtype=torch.int32, device="cuda")
+            n = torch.empty(1, dtype=torch.int32, device="cuda")
+            if i < 2:
+                plans[i].label(g[(k // 3 + i) % 3], out, n, stream=s)
+            else:
+                out, n = ccl.label(g[(k // 3 + i) % 3], stream=s)
+            outs.append(((k // 3 + i) % 3, out, n))
+    torch.cuda.synchronize()
+    for j, out, n in outs:
+        lo, no = want[j]
+        assert int(n.item()) == no
+        assert np.array_equal(out.cpu().numpy(), lo), j
