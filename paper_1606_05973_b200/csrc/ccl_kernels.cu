@@ -604,7 +604,11 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // in the list finish them per lane below.
     const int nmerge = sm.nmerge;
     constexpr int MLC = MR == MAXRUN ? MLCAP : 4 * MLCAP;
-    for (int i = threadIdx.x; i < min(nmerge, MLC); i += NW * 32) {
+    // One thread works through the list: with all 256 threads running Rem's
+    // splice concurrently, about 1 in 200 C3 runs lost a union (DESIGN.md
+    // "Open bug"); serial, 0 of 4000.
+    if (threadIdx.x == 0)
+    for (int i = 0; i < min(nmerge, MLC); i++) {
         const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
         if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
     }
