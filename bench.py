@@ -145,6 +145,116 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def make_roofline(ktimes, H, W, bh, ms, ws, peak, peak_src, workload):
+    """The path is HBM-bound by its algorithmic bytes (SURVEY.md section 8(d):
+    1 B read + 4 B written per pixel).  Top level = the dominant kernel (its
+    algorithmic bytes per launch / its average launch time, CUDA events on the
+    launch stream); `path` = the whole step against the peak.  At N > 1 every
+    figure is per GPU: this rank's band (bh rows) over the max-over-ranks step
+    time -- the per-GPU roofline % = 5*H*W / (n * B_peak * t) of SURVEY.md 8(d)."""
+    alg = ALG_BYTES_PER_PX["path"] * H * W
+    ach_gpu = alg / ws / (ms * 1e-3) / 1e9
+    kern = {}
+    for k, t in ktimes.items():
+        e = {"ms": t, "share": t / sum(ktimes.values())}
+        if ALG_BYTES_PER_PX.get(k):
+            e["algorithmic_bytes"] = ALG_BYTES_PER_PX[k] * bh * W
+            e["achieved_gbs"] = e["algorithmic_bytes"] / (t * 1e-3) / 1e9
+            e["frac"] = e["achieved_gbs"] / peak
+        if ws == 1:
+            tr = ncu_traffic(k, workload)
+            if tr is not None:
+                e["ncu_dram_bytes"] = tr
+            iss = ncu_issue(k, workload)
+            if iss is not None:
+                e["issue"] = iss
+        kern[k] = e
+    tr_all = [kern[k].get("ncu_dram_bytes") for k in kern if k in ALG_BYTES_PER_PX]
+    dom = max((k for k in ktimes if ALG_BYTES_PER_PX.get(k)), key=ktimes.get)
+    d = kern[dom]
+    r = {"bound": "hbm", "kernel": dom,
+         "achieved": d.get("achieved_gbs", 0.0), "peak": peak, "unit": "GB/s",
+         "frac": d.get("frac", 0.0), "traffic": d.get("ncu_dram_bytes"),
+         "algorithmic_bytes_per_launch": d.get("algorithmic_bytes", 0),
+         "peak_source": peak_src,
+         "path": {"achieved": ach_gpu, "frac": ach_gpu / peak,
+                  "algorithmic_bytes_per_step": alg // ws if ws > 1 else alg,
+                  "per_gpu": ws > 1,
+                  "traffic": sum(tr_all) if tr_all and all(t is not None for t in tr_all) else None},
+         "kernels": kern}
+    if ws > 1:
+        r["note"] = ("per GPU: rank 0's band; stage times from rank 0's ShardPlan events; "
+                     "xband_* stages = the cross-band protocol incl. its NCCL all-gathers")
+    # K1 moves 1 B/px of algorithmic bytes but is bound by instruction issue
+    # (shared-memory union-find, bit-parallel scans): its issue utilisation
+    # (ncu, committed summary) is reported beside the HBM roofline
+    iss = ncu_issue("k_tile_local", workload) if ws == 1 else None
+    if iss is not None:
+        r["issue"] = dict(iss, kernel="k_tile_local")
+    return r
+
+
+def cpu_model():
+    """Host CPU model name and logical core count (report the
+    box's host as measured)."""
+    name = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    name = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return name, os.cpu_count()
+
+
+def time_paremsp(img, runs):
+    """the multi-core host PARemSP (paremsp/, OpenMP, all
+    host cores), output checked against the oracle's by the caller."""
+    import paremsp
+    ts, out = [], None
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        out = paremsp.label(img)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), out
+
+
+def other_configs(dev, stream, reps=10):
+    """Single-image throughput on the other BASELINE.json configs (C1, C2,
+    C3, C5a-d): parity cases, reported beside the C4 bench line; each call
+    labels one device-resident image (CUDA events on the launch stream)."""
+    import torch
+    import synth
+    import paper_1606_05973_b200 as ccl
+    res = {}
+    for name in synth.CONFIGS:
+        if name == WORKLOAD:
+            continue
+        img = synth.generate(name)
+        H, W = img.shape
+        t = torch.from_numpy(img).to(dev)
+        plan = ccl.Plan(H, W, device=dev)
+        o = torch.empty((H, W), dtype=torch.int32, device=dev)
+        n = torch.empty(1, dtype=torch.int32, device=dev)
+        for _ in range(3):
+            plan.label(t, o, n)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            plan.label(t, o, n)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        res[name] = {"H": H, "W": W, "us_per_call": ms * 1e3, "gpx_s": H * W / (ms * 1e-3) / 1e9,
+                     "path_frac": 5 * H * W / (ms * 1e-3) / 1e9 / peak_hbm()[0],
+                     "n_components": int(n.item())}
+        del t, o, plan
+    return res
+
+
 def time_oracle(img, runs):
     import oracle
     ts, out = [], None
@@ -323,58 +433,21 @@ def main():
     n_gpu = int(n_out.item())
 
     peak, peak_src = peak_hbm()
-    roofline = None
-    if plan is not None:
-        # Per-kernel times: the same K steps again with CUDA events recorded on
-        # the launch stream between the kernels.  Kept out of the timed region
-        # above because events between kernels serialise the programmatic
-        # dependent launches the pipeline uses.
-        plan.set_profiling(args.steps)
-        for _ in range(args.steps):
-            step()
-        torch.cuda.synchronize(dev)
-        ktimes = plan.kernel_times()
-        plan.set_profiling(0)
-        # The path is HBM-bound by its algorithmic bytes (SURVEY.md section 8(d):
-        # 1 B read + 4 B written per pixel).  The top-level roofline is the
-        # dominant kernel's (its algorithmic bytes per launch / its average
-        # launch time, CUDA events on the launch stream); the whole step and
-        # every kernel's share are reported beside it.
-        alg = ALG_BYTES_PER_PX["path"] * H * W
-        ach = alg / (ms * 1e-3) / 1e9
-        dom = max(ktimes, key=ktimes.get)
-        kern = {}
-        for k, t in ktimes.items():
-            e = {"ms": t, "share": t / sum(ktimes.values())}
-            if ALG_BYTES_PER_PX.get(k):
-                e["algorithmic_bytes"] = ALG_BYTES_PER_PX[k] * H * W
-                e["achieved_gbs"] = e["algorithmic_bytes"] / (t * 1e-3) / 1e9
-                e["frac"] = e["achieved_gbs"] / peak
-            tr = ncu_traffic(k, args.workload)
-            if tr is not None:
-                e["ncu_dram_bytes"] = tr
-            kern[k] = e
-        tr_all = [ncu_traffic(k, args.workload) for k in ktimes]
-        d = kern[dom]
-        roofline = {"bound": "hbm", "kernel": dom,
-                    "achieved": d.get("achieved_gbs", 0.0), "peak": peak, "unit": "GB/s",
-                    "frac": d.get("frac", 0.0), "traffic": d.get("ncu_dram_bytes"),
-                    "algorithmic_bytes_per_launch": d.get("algorithmic_bytes", 0),
-                    "peak_source": peak_src,
-                    "path": {"achieved": ach, "frac": ach / peak, "algorithmic_bytes_per_step": alg,
-                             "traffic": sum(tr_all) if all(t is not None for t in tr_all) else None},
-                    "kernels": kern}
-        # K1 moves 1 B/px of algorithmic bytes but is bound by instruction
-        # issue (shared-memory union-find, bit-parallel scans): its issue
-        # utilisation is the roofline that binds it; every kernel's issue
-        # utilisation goes with its entry
-        for k in kern:
-            iss = ncu_issue(k, args.workload)
-            if iss is not None:
-                kern[k]["issue"] = iss
-        iss = ncu_issue("k_tile_local", args.workload)
-        if iss is not None:
-            roofline["issue"] = dict(iss, kernel="k_tile_local")
+    # Per-kernel (per-stage) times: the same K steps again with CUDA events
+    # recorded on the launch stream between the kernels.  Kept out of the
+    # timed region above because events between kernels serialise the
+    # programmatic dependent launches the pipeline uses.  At N > 1 every rank
+    # profiles its own band (ShardPlan); rank 0's times are reported.
+    prof = plan if plan is not None else splan
+    prof.set_profiling(args.steps)
+    if dist:
+        dist.barrier()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize(dev)
+    ktimes = prof.kernel_times()
+    prof.set_profiling(0)
+    roofline = make_roofline(ktimes, H, W, bh, ms, ws, peak, peak_src, args.workload)
 
     line = {
         "metric": METRIC, "value": value, "unit": "Gpx/s", "n_gpus": ws, "steps": args.steps,
@@ -391,6 +464,7 @@ def main():
     # of 64 per call (ccl_label_batch), device-resident, CUDA events
     if ws == 1 and plan is not None and not args.no_small:
         line["small_images"] = small_images(dev, stream)
+        line["other_configs"] = other_configs(dev, stream)
 
     # ---- end to end through the public API with host buffers (N=1)
     if ws == 1 and plan is not None and not args.no_e2e:
@@ -457,13 +531,25 @@ def main():
 
     # ---- CPU baseline (the oracle as it stands) + parity of the timed output
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu, ncpu = cpu_model()
         t, (lab_o, n_o) = time_oracle(img, args.cpu_runs)
         line["cpu_baseline"] = {"value": H * W / t / 1e9, "unit": "Gpx/s", "cores": 1, "kind": "oracle",
+                                "host_cpu": cpu, "host_logical_cores": ncpu,
                                 "sample": f"full {H}x{W} {args.workload} image, median of {args.cpu_runs} runs, "
                                           "single-threaded C oracle (ARemSP + canonical renumbering)"}
         if result_labels is not None:
             same = (n_o == n_gpu) and bool(np.array_equal(lab_o, result_labels))
             line["parity"] = {"vs": "oracle", "bit_exact": same, "n_components": n_gpu}
+        # the paper's own parallel design on all host cores
+        tp, (lab_p, n_p, used) = time_paremsp(img, args.cpu_runs)
+        line["cpu_baseline_paremsp"] = {
+            "value": H * W / tp / 1e9, "unit": "Gpx/s", "cores": used, "kind": "paremsp_openmp",
+            "host_cpu": cpu, "host_logical_cores": ncpu,
+            "bit_exact_vs_oracle": bool(n_p == n_o and np.array_equal(lab_p, lab_o)),
+            "sample": f"full {H}x{W} {args.workload} image, median of {args.cpu_runs} runs, PARemSP "
+                      "(paremsp/: OpenMP row chunks, locked boundary merger, parallel flatten + "
+                      "canonical renumbering)"}
+        del lab_p
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -5,6 +5,7 @@ to the GPU box with the repo snapshot).
   oracle    oracle/liboracle.so                    gcc             (test infrastructure)
   synth     synth/libsynth.so                      gcc + OpenMP    (seeded input generators)
   pins      tests/pins/libpins.so                  gcc             (brute force + validator)
+  paremsp   paremsp/libparemsp.so                  gcc + OpenMP    (multi-core host baseline)
 
 Usage: python build_native.py [product|oracle|synth|pins ...]   (default: all)
 """
@@ -57,6 +58,15 @@ def build_synth(force=False):
     if force or _stale(out, src):
         _run(["gcc", "-O3", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-Wall",
               "-o", out, src[0], "-lm"])
+    return out
+
+
+def build_paremsp(force=False):
+    src = [os.path.join(ROOT, "paremsp", "paremsp.c"), os.path.join(ROOT, "paremsp", "paremsp.h")]
+    out = os.path.join(ROOT, "paremsp", "libparemsp.so")
+    if force or _stale(out, src):
+        _run(["gcc", "-O3", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra",
+              "-o", out, src[0]])
     return out
 
 
@@ -115,14 +125,15 @@ def build_all(force=False):
     build_oracle(force)
     build_synth(force)
     build_pins(force)
+    build_paremsp(force)
     build_product(force)
 
 
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["oracle", "synth", "pins", "product"]
+    what = sys.argv[1:] or ["oracle", "synth", "pins", "paremsp", "product"]
     force = "-f" in what
     for w in what:
         if w == "-f":
             continue
-        {"oracle": build_oracle, "synth": build_synth, "pins": build_pins,
+        {"oracle": build_oracle, "synth": build_synth, "pins": build_pins, "paremsp": build_paremsp,
          "product": build_product}[w](force)

@@ -21,6 +21,13 @@
  *
  * Layout: row-major, pitch == W (bytes for img, int32 elements for labels).
  * Sizes: 1 <= H, 1 <= W, (int64)H*W <= INT32_MAX.
+ * Alignment: none required.  16-byte vector loads/stores are used only when
+ * W % 16 == 0 AND the img (loads) / labels (stores) base pointer is 16-byte
+ * aligned; otherwise the kernels fall back to narrower accesses.
+ *
+ * Ordering: the first kernel of a call waits for the previous work on
+ * `stream` (e.g. the caller's kernel that produced img) to complete before it
+ * reads any pixel.
  *
  * Ownership: the caller owns img, labels and n_components; the library never
  * frees or reallocates them.  labels must not alias img.  All workspace is
@@ -143,6 +150,20 @@ ccl_status ccl_plan_set_profiling(ccl_plan plan, int nsets);
 ccl_status ccl_plan_kernel_times(ccl_plan plan, const char **names, float *ms, int cap,
                                  int *count);
 
+/* ccl_plan_counters -- cumulative path counters of a plan (zeroed at
+ * ccl_plan_create), so a caller can tell which code paths of the tile-local
+ * scan (PAPER.md:865-930 Scan_ARemSP on a chunk) its
+ * images took:
+ *   out[0]  tiles whose strip-merge list overflowed (the per-row leftover
+ *           unions ran beside the list; > 1024 merges in a 32x1024 tile)
+ *   out[1]  tiles handed to the full-size pass (a tile row of > 256 runs)
+ *   out[2]  handed-over tiles whose merge list overflowed (> 256 merges)
+ *   out[3]  strip merges listed, all tiles
+ * Fills min(cap, *count) entries of `out` (HOST array; may be NULL with
+ * cap 0 to query *count).  Synchronizes the device (cudaMemcpy).
+ * Errors: CCL_INVALID_ARGUMENT for a NULL plan/count, CCL_CUDA_ERROR. */
+ccl_status ccl_plan_counters(ccl_plan plan, uint64_t *out, int cap, int *count);
+
 /* ------------------------------------------------------------------------
  * ccl_label_sharded -- one image split into contiguous row bands, one band
  * per rank of an NCCL communicator (the B200 analogue of PARemSP's row
@@ -171,6 +192,16 @@ ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_n
 ccl_status ccl_shard_plan_label(ccl_shard_plan plan, const uint8_t *band_img, int32_t *band_labels,
                                 int32_t *n_components, ccl_stream_t stream);
 ccl_status ccl_shard_plan_destroy(ccl_shard_plan plan);
+/* Per-stage CUDA-event profiling of a sharded plan (as ccl_plan_set_profiling /
+ * ccl_plan_kernel_times; events between the stages serialise the chained
+ * launches, so time profiled calls apart from throughput runs).  Stages:
+ * k_tile_local, k_border, xband_exchange (boundary-row roots, representatives,
+ * the key all-gather, slot unions, links), k_number, k_label, xband_export
+ * (count all-gather, band offset, boundary labels, label all-gather),
+ * k_fixup, k_write.  Local calls, not collective. */
+ccl_status ccl_shard_plan_set_profiling(ccl_shard_plan plan, int nsets);
+ccl_status ccl_shard_plan_kernel_times(ccl_shard_plan plan, const char **names, float *ms, int cap,
+                                       int *count);
 
 /* ------------------------------------------------------------------------
  * ccl_label_banded -- the row-band protocol of ccl_label_sharded run on ONE

@@ -56,6 +56,8 @@ _L.ccl_plan_set_profiling.restype = _i
 _L.ccl_plan_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p),
                                      ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(_i)]
 _L.ccl_plan_kernel_times.restype = _i
+_L.ccl_plan_counters.argtypes = [_vp, _u64p, _i, ctypes.POINTER(_i)]
+_L.ccl_plan_counters.restype = _i
 _L.ccl_label_sharded.argtypes = [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]
 _L.ccl_label_sharded.restype = _i
 _L.ccl_label_banded.argtypes = [_vp, _i, _i, _i, _vp, _vp, _vp]
@@ -68,6 +70,11 @@ _L.ccl_shard_plan_label.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _L.ccl_shard_plan_label.restype = _i
 _L.ccl_shard_plan_destroy.argtypes = [_vp]
 _L.ccl_shard_plan_destroy.restype = _i
+_L.ccl_shard_plan_set_profiling.argtypes = [_vp, _i]
+_L.ccl_shard_plan_set_profiling.restype = _i
+_L.ccl_shard_plan_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p),
+                                           ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(_i)]
+_L.ccl_shard_plan_kernel_times.restype = _i
 _L.ccl_nccl_get_unique_id.argtypes = [_vp]
 _L.ccl_nccl_get_unique_id.restype = _i
 _L.ccl_nccl_comm_create.argtypes = [_vp, _i, _i, ctypes.POINTER(_vp)]
@@ -109,6 +116,17 @@ def _check_img(img):
         raise ValueError("img must be contiguous (pitch == W)")
 
 
+def _check_out(out, n_out, shape, nmin, device):
+    """Caller-supplied output buffers: int32, contiguous, the right shape and
+    on the image's device (a wrong buffer would be an out-of-bounds write)."""
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.int32 or not out.is_contiguous() \
+            or tuple(out.shape) != tuple(shape) or out.device != device:
+        raise TypeError(f"out must be a contiguous int32 tensor of shape {tuple(shape)} on {device}")
+    if not isinstance(n_out, torch.Tensor) or n_out.dtype != torch.int32 or not n_out.is_contiguous() \
+            or n_out.numel() < nmin or n_out.device != device:
+        raise TypeError(f"n_out must be a contiguous int32 tensor of >= {nmin} elements on {device}")
+
+
 def label(img, out=None, n_out=None, stream=None, threshold=None):
     """Labels a 2-D uint8 CUDA image (foreground <=> != 0, or > `threshold`
     when given: ccl_label_threshold) with 8-connectivity.
@@ -121,6 +139,7 @@ def label(img, out=None, n_out=None, stream=None, threshold=None):
         out = torch.empty((H, W), dtype=torch.int32, device=img.device)
     if n_out is None:
         n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+    _check_out(out, n_out, (H, W), 1, img.device)
     if threshold is None:
         _check(_L.ccl_label(img.data_ptr(), H, W, out.data_ptr(), n_out.data_ptr(),
                             _stream_handle(stream)), "ccl_label")
@@ -143,6 +162,7 @@ def label_batch(imgs, out=None, n_out=None, stream=None):
         out = torch.empty((B, H, W), dtype=torch.int32, device=imgs.device)
     if n_out is None:
         n_out = torch.empty(B, dtype=torch.int32, device=imgs.device)
+    _check_out(out, n_out, (B, H, W), B, imgs.device)
     _check(_L.ccl_label_batch(imgs.data_ptr(), B, H, W, out.data_ptr(), n_out.data_ptr(),
                               _stream_handle(stream)), "ccl_label_batch")
     return out, n_out
@@ -156,7 +176,10 @@ class Plan:
     def __init__(self, H, W, device=None, batch=None):
         self.H, self.W = int(H), int(W)
         self.B = None if batch is None else int(batch)
-        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self._p = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             if self.B is None:
@@ -181,10 +204,13 @@ class Plan:
             raise TypeError("img must be a contiguous torch.uint8 CUDA tensor")
         if tuple(img.shape) != shape:
             raise ValueError(f"plan is for {shape}, got {tuple(img.shape)}")
+        if img.device != self.device:
+            raise ValueError(f"plan lives on {self.device}, img is on {img.device}")
         if out is None:
             out = torch.empty(shape, dtype=torch.int32, device=img.device)
         if n_out is None:
             n_out = torch.empty(1 if self.B is None else self.B, dtype=torch.int32, device=img.device)
+        _check_out(out, n_out, shape, 1 if self.B is None else self.B, img.device)
         _check(_L.ccl_plan_label(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
                                  _stream_handle(stream)), "ccl_plan_label")
         return out, n_out
@@ -195,6 +221,10 @@ class Plan:
         for t, dt in ((img, torch.uint8), (out, torch.int32), (n_out, torch.int32)):
             if t.is_cuda or t.dtype != dt or not t.is_contiguous():
                 raise TypeError("label_host takes contiguous host tensors (uint8 img, int32 out/n)")
+        shape = (self.H, self.W) if self.B is None else (self.B, self.H, self.W)
+        nb = 1 if self.B is None else self.B
+        if tuple(img.shape) != shape or tuple(out.shape) != shape or n_out.numel() < nb:
+            raise ValueError(f"plan is for {shape} (n_out >= {nb} elements)")
         _check(_L.ccl_plan_label_host(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
                                       _stream_handle(stream)), "ccl_plan_label_host")
         return out, n_out
@@ -213,6 +243,16 @@ class Plan:
         n = ctypes.c_int()
         _check(_L.ccl_plan_kernel_times(self._p, names, ms, cap, ctypes.byref(n)), "ccl_plan_kernel_times")
         return {names[i].decode(): float(ms[i]) for i in range(n.value)}
+
+    def counters(self):
+        """Cumulative path counters of the plan (ccl_plan_counters): which code
+        paths of the tile-local scan its images took."""
+        cap = 8
+        buf = (ctypes.c_uint64 * cap)()
+        n = ctypes.c_int()
+        _check(_L.ccl_plan_counters(self._p, buf, cap, ctypes.byref(n)), "ccl_plan_counters")
+        keys = ["k1_list_overflow", "k1_handover", "k1big_list_overflow", "k1_merges"]
+        return {keys[i] if i < len(keys) else f"c{i}": int(buf[i]) for i in range(min(n.value, cap))}
 
     def close(self):
         if self._p:
@@ -260,6 +300,7 @@ def label_sharded(band_img, row0, H_total, comm, out=None, n_out=None, stream=No
         out = torch.empty((bh, W), dtype=torch.int32, device=band_img.device)
     if n_out is None:
         n_out = torch.empty(1, dtype=torch.int32, device=band_img.device)
+    _check_out(out, n_out, (bh, W), 1, band_img.device)
     _check(_L.ccl_label_sharded(band_img.data_ptr(), bh, W, int(row0), int(H_total), out.data_ptr(),
                                 n_out.data_ptr(), comm.handle, _stream_handle(stream)),
            "ccl_label_sharded")
@@ -276,6 +317,7 @@ def label_banded(img, nbands, out=None, n_out=None, stream=None):
         out = torch.empty((H, W), dtype=torch.int32, device=img.device)
     if n_out is None:
         n_out = torch.empty(1, dtype=torch.int32, device=img.device)
+    _check_out(out, n_out, (H, W), 1, img.device)
     _check(_L.ccl_label_banded(img.data_ptr(), H, W, int(nbands), out.data_ptr(), n_out.data_ptr(),
                                _stream_handle(stream)), "ccl_label_banded")
     return out, n_out
@@ -315,9 +357,24 @@ class ShardPlan:
             out = torch.empty((self.band_H, self.W), dtype=torch.int32, device=band_img.device)
         if n_out is None:
             n_out = torch.empty(1, dtype=torch.int32, device=band_img.device)
+        _check_out(out, n_out, (self.band_H, self.W), 1, band_img.device)
         _check(_L.ccl_shard_plan_label(self._p, band_img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
                                        _stream_handle(stream)), "ccl_shard_plan_label")
         return out, n_out
+
+    def set_profiling(self, nsets=1):
+        """Record per-stage CUDA events for the next label() calls (0 disables)."""
+        _check(_L.ccl_shard_plan_set_profiling(self._p, int(nsets)), "ccl_shard_plan_set_profiling")
+
+    def kernel_times(self):
+        """{stage name: ms} averaged over the profiled calls (this rank)."""
+        cap = 16
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int()
+        _check(_L.ccl_shard_plan_kernel_times(self._p, names, ms, cap, ctypes.byref(n)),
+               "ccl_shard_plan_kernel_times")
+        return {names[i].decode(): float(ms[i]) for i in range(n.value)}
 
     def close(self):
         if self._p:

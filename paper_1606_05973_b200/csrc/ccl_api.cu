@@ -37,7 +37,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
 
 enum {
     A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
-    A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_K1OVER, A_COUNT
+    A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_K1OVER, A_STATS, A_COUNT
 };
 
 void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
@@ -63,6 +63,7 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         16,                             // ticket
         (size_t)g.nTy * 4,              // rowexcl
         (nT + 1) * 4,                   // k1over + its count
+        STAT_COUNT * 8,                 // stats
     };
     size_t o = 0;
     for (int i = 0; i < A_COUNT; i++) {
@@ -98,13 +99,16 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.rowexcl = reinterpret_cast<int32_t *>(b + offs[A_ROWEXCL]);
     w.k1over = reinterpret_cast<int32_t *>(b + offs[A_K1OVER]);
     w.k1over_n = w.k1over + g.nT;
+    w.stats = reinterpret_cast<unsigned long long *>(b + offs[A_STATS]);
     w.xlab = nullptr;
     w.boff = nullptr;
     return w;
 }
 
 cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream) {
-    return cudaMemsetAsync(ws.k1over_n, 0, sizeof(int32_t), stream);
+    cudaError_t e = cudaMemsetAsync(ws.k1over_n, 0, sizeof(int32_t), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws.stats, 0, STAT_COUNT * sizeof(unsigned long long), stream);
+    return e;
 }
 
 }  // namespace cclb
@@ -332,6 +336,16 @@ ccl_status ccl_plan_kernel_times(ccl_plan p, const char **names, float *ms, int 
         }
         ms[i] = (float)(acc / nset);
     }
+    return CCL_OK;
+}
+
+ccl_status ccl_plan_counters(ccl_plan p, uint64_t *out, int cap, int *count) {
+    if (!p || !count) return CCL_INVALID_ARGUMENT;
+    *count = STAT_COUNT;
+    if (!out || cap <= 0) return CCL_OK;
+    unsigned long long h[STAT_COUNT];
+    if (cudaMemcpy(h, p->ws.stats, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return CCL_CUDA_ERROR;
+    for (int i = 0; i < STAT_COUNT && i < cap; i++) out[i] = h[i];
     return CCL_OK;
 }
 

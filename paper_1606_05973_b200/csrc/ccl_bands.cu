@@ -184,10 +184,19 @@ ccl_status xband_init(XBand &x, int nb, int W) {
 }
 
 // A: local labeling; slot keys / nodes / representatives into (keys, reps)
+// Profiling events of a band step (ShardPlan profiling), SHARD_EV per set:
+// 0 K1, 1 K2, 2 cross-band exchange (row roots, representatives,
+// all-gather, slot unions, links), 3 K3, 4 K3b, 5 count all-gather + export
+// + label all-gather, 6 K4, 7 K5, 8 end.
+constexpr int SHARD_EV = 9;
+const char *const kShardNames[SHARD_EV - 1] = {"k_tile_local", "k_border", "xband_exchange", "k_number",
+                                                "k_label", "xband_export", "k_fixup", "k_write"};
+
 ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, int32_t *spar, int spar_lo,
-                        int spar_hi, cudaStream_t s) {
+                        int spar_hi, cudaStream_t s, cudaEvent_t *ev = nullptr) {
     const int W = b.g.W;
-    CK(run_stage_local(b.g, b.ws, img, s, nullptr));
+    CK(run_stage_local(b.g, b.ws, img, s, ev));
+    if (ev) CK(cudaEventRecord(ev[2], s));
     CK(band_row_roots(b.g, b.ws, keys, b.d_nodes, s));
     CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, spar, spar_lo, spar_hi, s));
     return CCL_OK;
@@ -195,9 +204,10 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
 
 // B (after the slot tables are complete): link this band's components whose
 // class starts elsewhere.  C: roots + numbering scan -> N_band in counts[self].
-ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s) {
+ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s,
+                         cudaEvent_t *ev = nullptr) {
     CK(band_link(b.ws, x.W, self, x.keys, x.spar, b.d_nodes, s));
-    CK(run_stage_count(b.g, b.ws, count_out, s, nullptr));
+    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 1 : nullptr));  // ev[3], ev[4]
     return CCL_OK;
 }
 
@@ -209,9 +219,9 @@ ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int
 }
 
 // E: labels of merged components (foreign ones from the exported table) + write
-ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s) {
+ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s, cudaEvent_t *ev = nullptr) {
     b.ws.xlab = x.exps;
-    CK(run_stage_final(b.g, b.ws, labels, s, nullptr));
+    CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 2 : nullptr));  // ev[6], ev[7], ev[8]
     return CCL_OK;
 }
 
@@ -277,39 +287,64 @@ struct ccl_shard_plan_st {
     XBand x;
     ncclComm_t comm = nullptr;
     int nranks = 0, rank = 0, W = 0;
+    int prof_sets = 0;          // profiling ring size (0 = off)
+    cudaEvent_t *ev = nullptr;  // prof_sets * SHARD_EV events
+    long long prof_calls = 0;
+    void free_events() {
+        if (ev) {
+            for (int i = 0; i < prof_sets * SHARD_EV; i++)
+                if (ev[i]) cudaEventDestroy(ev[i]);
+            delete[] ev;
+        }
+        ev = nullptr;
+        prof_sets = 0;
+        prof_calls = 0;
+    }
+    ~ccl_shard_plan_st() { free_events(); }
 };
 
 extern "C" {
 
-ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_nccl_comm_t comm_,
-                                 ccl_stream_t stream, ccl_shard_plan *plan_out) {
-    if (!plan_out) return CCL_INVALID_ARGUMENT;
+// The argument check is collective: every rank's (band_H, row0, W, H_total,
+// local verdict) is all-gathered BEFORE any rank returns, so a rank with bad
+// arguments makes every rank return CCL_INVALID_ARGUMENT / CCL_TOO_LARGE
+// instead of leaving the others blocked in the all-gather.  `extra` is the
+// caller's own local verdict (e.g. the buffer checks of ccl_label_sharded).
+static ccl_status shard_plan_create(int band_H, int W, int row0, int H_total, ccl_nccl_comm_t comm_,
+                                    ccl_stream_t stream, ccl_status extra, ccl_shard_plan *plan_out) {
+    if (!plan_out) return CCL_INVALID_ARGUMENT;  // (no communicator use is possible without a result slot)
     *plan_out = nullptr;
-    if (!comm_ || band_H < 1 || W < 1 || row0 < 0 || H_total < 1 || row0 + band_H > H_total)
-        return CCL_INVALID_ARGUMENT;
-    if ((int64_t)H_total * W > INT32_MAX) return CCL_TOO_LARGE;
+    if (!comm_) return CCL_INVALID_ARGUMENT;     // no collective without a communicator
+    ccl_status local = extra;
+    if (local == CCL_OK && (band_H < 1 || W < 1 || row0 < 0 || H_total < 1 || row0 + band_H > H_total))
+        local = CCL_INVALID_ARGUMENT;
+    if (local == CCL_OK && (int64_t)H_total * W > INT32_MAX) local = CCL_TOO_LARGE;
     ncclComm_t comm = reinterpret_cast<ncclComm_t>(comm_);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int nranks = 0, rank = 0;
     CKN(ncclCommCount(comm, &nranks));
     CKN(ncclCommUserRank(comm, &rank));
-    // collective argument check: every rank's (band_H, row0, W, H_total)
+    // collective argument check: every rank's (band_H, row0, W, H_total, status)
+    constexpr int NM = 5;
     int32_t *d_meta = nullptr;
-    CK(cudaMalloc(&d_meta, sizeof(int32_t) * 4 * (nranks + 1)));
-    int32_t mine[4] = {band_H, row0, W, H_total};
+    CK(cudaMalloc(&d_meta, sizeof(int32_t) * NM * (nranks + 1)));
+    int32_t mine[NM] = {band_H, row0, W, H_total, (int32_t)local};
     CK(cudaMemcpyAsync(d_meta, mine, sizeof(mine), cudaMemcpyHostToDevice, s));
-    CKN(ncclAllGather(d_meta, d_meta + 4, 4, ncclInt32, comm, s));
-    std::vector<int32_t> meta(4 * (size_t)nranks);
-    CK(cudaMemcpyAsync(meta.data(), d_meta + 4, sizeof(int32_t) * 4 * nranks, cudaMemcpyDeviceToHost, s));
+    CKN(ncclAllGather(d_meta, d_meta + NM, NM, ncclInt32, comm, s));
+    std::vector<int32_t> meta(NM * (size_t)nranks);
+    CK(cudaMemcpyAsync(meta.data(), d_meta + NM, sizeof(int32_t) * NM * nranks, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     cudaFree(d_meta);
-    int acc = 0;
+    int64_t acc = 0;
     bool ok = true;
+    ccl_status worst = CCL_OK;
     for (int k = 0; k < nranks; k++) {
-        ok = ok && meta[4 * k + 1] == acc && meta[4 * k + 2] == W && meta[4 * k + 3] == H_total &&
-             meta[4 * k] >= 1;
-        acc += meta[4 * k];
+        const int32_t *m = &meta[(size_t)NM * k];
+        if (m[4] != CCL_OK && worst == CCL_OK) worst = (ccl_status)m[4];
+        ok = ok && m[1] == acc && m[2] == W && m[3] == H_total && m[0] >= 1;
+        acc += m[0];
     }
+    if (worst != CCL_OK) return worst;
     if (!ok || acc != H_total) return CCL_INVALID_ARGUMENT;
     ccl_shard_plan p = new (std::nothrow) ccl_shard_plan_st;
     if (!p) return CCL_OUT_OF_MEMORY;
@@ -327,6 +362,11 @@ ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_n
     return CCL_OK;
 }
 
+ccl_status ccl_shard_plan_create(int band_H, int W, int row0, int H_total, ccl_nccl_comm_t comm_,
+                                 ccl_stream_t stream, ccl_shard_plan *plan_out) {
+    return shard_plan_create(band_H, W, row0, H_total, comm_, stream, CCL_OK, plan_out);
+}
+
 ccl_status ccl_shard_plan_destroy(ccl_shard_plan p) {
     if (!p) return CCL_INVALID_ARGUMENT;
     delete p;
@@ -341,9 +381,14 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     XBand &x = p->x;
     const size_t slots = 2 * (size_t)p->W;
     const int self = p->rank;
+    cudaEvent_t *ev = nullptr;
+    if (p->prof_sets > 0) {
+        ev = p->ev + (p->prof_calls % p->prof_sets) * SHARD_EV;
+        p->prof_calls++;
+    }
     // A + X1 (own slots written in place, then gathered)
     ccl_status st = band_phase_a(b, band_img, x.keys + self * slots, x.reps + self * slots, x.spar, 0,
-                                 (int)(p->nranks * slots), s);
+                                 (int)(p->nranks * slots), s, ev);
     if (st != CCL_OK) return st;
     CKN(ncclGroupStart());
     CKN(ncclAllGather(x.keys + self * slots, x.keys, slots, ncclInt64, p->comm, s));
@@ -351,23 +396,60 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     CKN(ncclGroupEnd());
     // B + C + X2
     CK(band_resolve(p->nranks, p->W, x.keys, x.reps, x.spar, s));
-    if ((st = band_phase_bc(b, x, self, x.counts + self, s)) != CCL_OK) return st;
+    if ((st = band_phase_bc(b, x, self, x.counts + self, s, ev)) != CCL_OK) return st;
+    if (ev) CK(cudaEventRecord(ev[5], s));
     CKN(ncclAllGather(x.counts + self, x.counts, 1, ncclInt32, p->comm, s));
     // D + X3
     if ((st = band_phase_d(b, x, self, n_components, x.exps + self * slots, s)) != CCL_OK) return st;
     CKN(ncclAllGather(x.exps + self * slots, x.exps, slots, ncclInt32, p->comm, s));
     // E
-    return band_phase_e(b, x, band_labels, s);
+    return band_phase_e(b, x, band_labels, s, ev);
+}
+
+ccl_status ccl_shard_plan_set_profiling(ccl_shard_plan p, int nsets) {
+    if (!p || nsets < 0) return CCL_INVALID_ARGUMENT;
+    p->free_events();
+    if (nsets == 0) return CCL_OK;
+    p->ev = new (std::nothrow) cudaEvent_t[(size_t)nsets * SHARD_EV]();
+    if (!p->ev) return CCL_OUT_OF_MEMORY;
+    p->prof_sets = nsets;
+    for (int i = 0; i < nsets * SHARD_EV; i++)
+        if (cudaEventCreate(&p->ev[i]) != cudaSuccess) return CCL_CUDA_ERROR;
+    return CCL_OK;
+}
+
+ccl_status ccl_shard_plan_kernel_times(ccl_shard_plan p, const char **names, float *ms, int cap, int *count) {
+    if (!p || !count) return CCL_INVALID_ARGUMENT;
+    *count = SHARD_EV - 1;
+    if (p->prof_sets == 0 || p->prof_calls == 0) return CCL_INVALID_ARGUMENT;
+    const int nset = (int)(p->prof_calls < p->prof_sets ? p->prof_calls : p->prof_sets);
+    for (int i = 0; i < SHARD_EV - 1 && i < cap; i++) {
+        if (names) names[i] = kShardNames[i];
+        if (!ms) continue;
+        double acc = 0;
+        for (int k = 0; k < nset; k++) {
+            cudaEvent_t *e = p->ev + (size_t)k * SHARD_EV;
+            if (cudaEventSynchronize(e[i + 1]) != cudaSuccess) return CCL_CUDA_ERROR;
+            float t = 0;
+            if (cudaEventElapsedTime(&t, e[i], e[i + 1]) != cudaSuccess) return CCL_CUDA_ERROR;
+            acc += t;
+        }
+        ms[i] = (float)(acc / nset);
+    }
+    return CCL_OK;
 }
 
 ccl_status ccl_label_sharded(const uint8_t *band_img, int band_H, int W, int row0, int H_total,
                              int32_t *band_labels, int32_t *n_components, ccl_nccl_comm_t comm,
                              ccl_stream_t stream) {
-    if (!band_img || !band_labels || !n_components) return CCL_INVALID_ARGUMENT;
+    const ccl_status local = (!band_img || !band_labels || !n_components) ? CCL_INVALID_ARGUMENT : CCL_OK;
     ccl_shard_plan p = nullptr;
-    ccl_status st = ccl_shard_plan_create(band_H, W, row0, H_total, comm, stream, &p);
+    ccl_status st = shard_plan_create(band_H, W, row0, H_total, comm, stream, local, &p);
     if (st != CCL_OK) return st;
     st = ccl_shard_plan_label(p, band_img, band_labels, n_components, stream);
+    // the plan's buffers are freed next: the enqueued work must be done with them
+    if (cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess && st == CCL_OK)
+        st = CCL_CUDA_ERROR;
     ccl_shard_plan_destroy(p);
     return st;
 }

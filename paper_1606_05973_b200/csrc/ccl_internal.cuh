@@ -64,6 +64,7 @@ struct Workspace {
     int32_t *rowexcl;     // [nTy]             labels of earlier tile rows
     int32_t *k1over;      // [nT]              tiles K1 handed to its full-size pass
     int32_t *k1over_n;    // [1]               their count (0 between calls; K3 resets it)
+    unsigned long long *stats;  // [STAT_COUNT]  cumulative path counters (ccl_plan_counters)
     // row bands only (null for a whole image):
     const int32_t *xlab;  // [nb*2W]           exported labels of all bands' boundary slots; a
                           //                   node whose parent is -2-f takes xlab[f]
@@ -94,6 +95,16 @@ Workspace workspace_bind(const Geometry &g, void *base);
 // Zeroes the counters a new workspace must start with (before its first call).
 cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream);
 
+
+// Path counters (cumulative over a plan's calls; zeroed by workspace_init):
+// which K1 code paths the tiles took, so tests can prove the dense paths ran.
+enum {
+    STAT_K1_LIST_OVERFLOW = 0,  // k_tile_local tiles whose strip-merge list overflowed (per-row leftover pass)
+    STAT_K1_HANDOVER,           // tiles k_tile_local handed to k_tile_big (a row of > 256 runs)
+    STAT_K1BIG_LIST_OVERFLOW,   // k_tile_big tiles whose merge list overflowed
+    STAT_K1_MERGES,             // strip merges listed (all tiles, both passes)
+    STAT_COUNT
+};
 
 enum { K_TILE = 0, K_BORDER, K_NUMBER, K_LABEL, K_FIXUP, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];

@@ -173,42 +173,47 @@ __device__ __forceinline__ int leftmost3(uint32_t w, uint32_t wp, uint32_t wn, i
 }
 
 // ---------------------------------------------------------------- union-find
-// Lock-free Rem's union with splicing on a shared-memory parent array in
-// which parent < child for every non-root (labels are created in raster
-// order).  This is the paper's merge run concurrently the
-// way its merger does: the root link is an atomicCAS
-// (the role of merger's lock + "still a root?" re-check)
-// and the splice (unlocked in merger) is a CAS that only
-// lowers p[x].  Every value stored into p[x] is smaller than x: no cycles.
-__device__ void merge_smem(uint16_t *p, uint32_t x, uint32_t y) {
-    volatile uint16_t *vp = p;
+// Lock-free union on a shared-memory parent array in which parent < child for
+// every non-root (labels are created in raster order).  This replaces the
+// paper's Rem's merge with splicing as its parallel merger
+// runs it (lock the root, re-check it is still a root,
+// link; the splice is unlocked).  On the GPU the splice is what breaks: it
+// moves a subtree from one tree into another before the two trees are joined,
+// so for a moment a set is split, and a concurrent merge that reads through
+// the split can stop early (round 1 lost about 1 union in 150 C3 runs that
+// way).  Here p changes only by
+//   (link)     atomicCAS(p[r], r, s): a root r goes under s < r; the CAS
+//              succeeds only while r is still a root (merger's re-check);
+//   (halving)  p[x] <- p[p[x]] for a non-root x: an ancestor of x.
+// Neither moves a node out of its tree, so trees (the sets) only ever merge,
+// and p[x] <= x always holds (no cycles).  union(a, b) returns only when
+// find(a) == find(b) was observed (trees only grow: they are joined from then
+// on) or after its own successful link; a failed CAS means another link
+// succeeded (lock-free).  The root of a set is its minimum index = its first
+// run in raster order, as with Rem's min-linking (DESIGN.md "Tile-local
+// union").
+__device__ __forceinline__ uint32_t find_smem(volatile uint16_t *vp, uint32_t x) {
     while (true) {
-        uint32_t px = vp[x], py = vp[y];
-        if (px == py) return;
-        if (px < py) {
-            uint32_t t = x; x = y; y = t;
-            t = px; px = py; py = t;
-        }
-        // now p[x] > p[y]
-        if (px == x) {
-            if (atomicCAS(reinterpret_cast<unsigned short *>(p + x), (unsigned short)x,
-                          (unsigned short)py) == (unsigned short)x)
-                return;
-            continue;  // x stopped being a root meanwhile: retry from x
-        }
-        // splice: x's subtree becomes a sibling under py.  Done with a CAS
-        // that only ever lowers p[x]; an unconditional store can raise p[x]
-        // over a concurrent splice, and that lost rare unions in testing.
-        {
-            unsigned short cur = (unsigned short)px;
-            while (true) {
-                const unsigned short o =
-                    atomicCAS(reinterpret_cast<unsigned short *>(p + x), cur, (unsigned short)py);
-                if (o == cur || o <= py) break;
-                cur = o;
-            }
-        }
-        x = px;
+        const uint32_t px = vp[x];
+        if (px == x) return x;
+        const uint32_t ppx = vp[px];
+        if (ppx == px) return px;
+        vp[x] = (uint16_t)ppx;  // path halving: x is not a root, ppx is its ancestor
+        x = ppx;
+    }
+}
+__device__ __forceinline__ void union_smem(uint16_t *p, uint32_t a, uint32_t b) {
+    volatile uint16_t *vp = p;
+    a = find_smem(vp, a);
+    b = find_smem(vp, b);
+    while (a != b) {
+        if (a < b) { const uint32_t t = a; a = b; b = t; }
+        // a > b: link the root a under b while a is still a root
+        const uint32_t o = atomicCAS(reinterpret_cast<unsigned short *>(p + a), (unsigned short)a,
+                                     (unsigned short)b);
+        if (o == a) return;
+        a = find_smem(vp, o);  // a was linked meanwhile: continue from its new root
+        b = find_smem(vp, b);
     }
 }
 
@@ -430,6 +435,17 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             }
         }
     }
+    // The tiles of the first quarter wave are nobody's look-ahead: they warm
+    // their own lines.  (Prefetches may run before the grid dependency wait:
+    // they only move lines into L2, the coherence point.)
+    if (tile < pfd) {
+        const int prow = R0 + (threadIdx.x >> 3), pcol = C0 + (threadIdx.x & 7) * 128;
+        if ((int)(threadIdx.x >> 3) < rows && pcol < g.W)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(img + (int64_t)prow * g.W + pcol));
+    }
+    // The image may be written by the kernel just before this one on the
+    // stream (the caller's producer): no pixel is loaded before the wait.
+    pdl_wait();
     // ---- P0: the pixels of the tile, read once with 16-byte streaming loads:
     // fg = byte != 0 (reading A10) -- or byte > thr when a
     // threshold is set -- one bit per pixel.  The warp's S rows are all in
@@ -465,7 +481,6 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         for (int i = 0; i < S; i++)
             xs[i] = (r0 + i < rows && gword < g.WW) ? load_word<THR>(img, g, R0 + r0 + i, 32 * gword) : 0u;
     }
-    pdl_wait();  // the previous call's kernels are done with the workspace
     // bm (1/8 B per pixel) is read again by K2 and K5 while ~5 B/px of image
     // and labels stream through L2: it is stored with the evict_last priority
     // (K5's label stores are evict_first), measured -10 us on C4
@@ -521,7 +536,10 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     }
     if (MR < MAXRUN) {
         if (__syncthreads_or(over)) {  // too many runs in a row: k_tile_big takes the tile
-            if (threadIdx.x == 0) ws.k1over[atomicAdd(ws.k1over_n, 1)] = tile;
+            if (threadIdx.x == 0) {
+                ws.k1over[atomicAdd(ws.k1over_n, 1)] = tile;
+                atomicAdd(ws.stats + STAT_K1_HANDOVER, 1ull);
+            }
             return;
         }
     } else {
@@ -604,13 +622,15 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // in the list finish them per lane below.
     const int nmerge = sm.nmerge;
     constexpr int MLC = MR == MAXRUN ? MLCAP : 4 * MLCAP;
-    // One thread works through the list: with all 256 threads running Rem's
-    // splice concurrently, about 1 in 200 C3 runs lost a union (DESIGN.md
-    // "Open bug"); serial, 0 of 4000.
-    if (threadIdx.x == 0)
-    for (int i = 0; i < min(nmerge, MLC); i++) {
+    if (threadIdx.x == 0 && nmerge > 0) {  // path counters (ccl_plan_counters)
+        atomicAdd(ws.stats + STAT_K1_MERGES, (unsigned long long)nmerge);
+        if (nmerge > MLC) atomicAdd(ws.stats + (MR == MAXRUN ? STAT_K1BIG_LIST_OVERFLOW : STAT_K1_LIST_OVERFLOW), 1ull);
+    }
+    // All 256 threads work through the list at once (union_smem is safe
+    // under concurrency, see above).
+    for (int i = threadIdx.x; i < min(nmerge, MLC); i += NW * 32) {
         const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
-        if (vp[a] != vp[c]) merge_smem(sm.p, a, c);
+        if (vp[a] != vp[c]) union_smem(sm.p, a, c);
     }
     if (nmerge <= MLC) {  // nothing left per lane: clear the rows for bbits
 #pragma unroll
@@ -634,7 +654,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             const int a = ub + __popc(hu & upto(b)) - 1;  // the upper run with head h
             // the lower run containing pixel h-1
             const int c = xb - 1 + __popc(hx & ((1u << b) - 1u));
-            if (vp[a] != vp[c]) merge_smem(sm.p, (uint32_t)a, (uint32_t)c);
+            if (vp[a] != vp[c]) union_smem(sm.p, (uint32_t)a, (uint32_t)c);
         }
     }
     __syncthreads();
@@ -1504,8 +1524,18 @@ static cudaError_t set_attrs() {
     return cudaSuccess;
 }
 
-cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
+// 16-byte vector loads (K1) and stores (K5) need the row pitch AND the base
+// pointer 16-byte aligned; g.aligned holds the pitch test, the pointer is
+// checked per call.
+static Geometry with_ptr_alignment(const Geometry &g0, const void *ptr) {
+    Geometry g = g0;
+    g.aligned = g0.aligned && ((reinterpret_cast<uintptr_t>(ptr) & 15u) == 0);
+    return g;
+}
+
+cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8_t *img,
                             cudaStream_t stream, cudaEvent_t *ev) {
+    const Geometry g = with_ptr_alignment(g0, img);
     cudaError_t e = set_attrs();
     if (e != cudaSuccess) return e;
     auto mark = [&](int i) {
@@ -1545,8 +1575,9 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
     return cudaGetLastError();
 }
 
-cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+cudaError_t run_stage_final(const Geometry &g0, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev) {
+    const Geometry g = with_ptr_alignment(g0, labels);
     auto mark = [&](int i) {
         if (ev) cudaEventRecord(ev[i], stream);
     };

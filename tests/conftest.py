@@ -21,4 +21,5 @@ def _native_built():
     build_native.build_oracle()
     build_native.build_synth()
     build_native.build_pins()
+    build_native.build_paremsp()
     yield

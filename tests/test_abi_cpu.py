@@ -81,7 +81,10 @@ def test_argument_validation_without_gpu(lib):
     assert lib.ccl_plan_set_threshold(None, 127) == 1
     lib.ccl_label_sharded.argtypes = [vp, i, i, i, i, vp, vp, vp, vp]
     assert lib.ccl_label_sharded(fake, 4, 4, 0, 4, other, n, None, None) == 1  # no comm
-    assert lib.ccl_label_sharded(fake, 4, 4, 2, 4, other, n, fake, None) == 1  # band past H_total
+    assert lib.ccl_label_sharded(fake, 0, 4, 0, 4, other, n, None, None) == 1  # no comm, band_H < 1
+    # (with a communicator the shape checks are collective -- every rank's
+    # verdict is all-gathered first -- so they are tested on the GPU:
+    # tests/test_gpu_bands.py::test_sharded_bad_arguments_are_collective)
 
 
 def test_python_binding_imports_and_fails_loudly_without_library(tmp_path):

@@ -88,3 +88,26 @@ def test_bands_with_handed_over_tiles(nb):
     lb, nb_ = banded(img, nb)
     lo, no = oracle.label(img)
     assert nb_ == no and np.array_equal(lb, lo)
+
+
+def test_sharded_bad_arguments_are_collective():
+    """Argument checks of the sharded calls go through the all-gather (every
+    rank's verdict), so a bad rank cannot leave the others blocked; with one
+    rank the bad call simply returns CCL_INVALID_ARGUMENT / CCL_TOO_LARGE and
+    the communicator stays usable."""
+    import ctypes
+    uid = ccl.nccl_unique_id()
+    comm = ccl.NcclComm(uid, 1, 0)
+    L = ccl._L
+    vp = ctypes.c_void_p
+    t = torch.zeros((4, 4), dtype=torch.uint8, device="cuda")
+    o = torch.zeros((4, 4), dtype=torch.int32, device="cuda")
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = vp(torch.cuda.current_stream().cuda_stream)
+    assert L.ccl_label_sharded(t.data_ptr(), 4, 4, 2, 4, o.data_ptr(), n.data_ptr(), comm.handle, s) == 1  # past H_total
+    assert L.ccl_label_sharded(t.data_ptr(), 4, 4, 0, 5, o.data_ptr(), n.data_ptr(), comm.handle, s) == 1  # rows != H_total
+    assert L.ccl_label_sharded(None, 4, 4, 0, 4, o.data_ptr(), n.data_ptr(), comm.handle, s) == 1          # null image
+    assert L.ccl_label_sharded(t.data_ptr(), 4, 4, 0, 4, o.data_ptr(), n.data_ptr(), comm.handle, s) == 0  # still usable
+    torch.cuda.synchronize()
+    assert int(n.item()) == 0
+    comm.close()

@@ -34,6 +34,114 @@ def test_repeated_runs_bit_exact(name, reps):
     assert not bad, f"{name}: runs {bad} of {reps} differ from the oracle"
 
 
+def _handed_over_dense(H=512, W=4096, seed=11):
+    """Bernoulli(0.6) with alternating rows spliced in (not isolated): tiles
+    with a row of > 256 runs go to the full-size K1 pass, and their alternating
+    rows merge with the dense rows around them (> 256 strip merges)."""
+    img = synth.bernoulli(H, W, 0.6, seed=seed)
+    for r in range(5, H - 1, 13):
+        # three alternating rows: the middle one keeps all 2048 single-pixel
+        # runs (its holes are not bridged from above or below)
+        img[r - 1:r + 2] = 0
+        img[r - 1:r + 2, ::2] = 1
+    return img
+
+
+def _stress(img_or_stack, reps, batch=None):
+    if batch:
+        want = [oracle.label(im) for im in img_or_stack]
+        ref = torch.from_numpy(np.stack([w[0] for w in want])).cuda()
+        nref = torch.tensor([w[1] for w in want], dtype=torch.int32, device="cuda")
+        t = torch.from_numpy(np.ascontiguousarray(np.stack(img_or_stack))).cuda()
+        plan = ccl.Plan(*img_or_stack[0].shape, batch=len(img_or_stack))
+        n = torch.empty(len(img_or_stack), dtype=torch.int32, device="cuda")
+    else:
+        lo, no = oracle.label(img_or_stack)
+        ref = torch.from_numpy(lo).cuda()
+        nref = torch.tensor([no], dtype=torch.int32, device="cuda")
+        t = torch.from_numpy(img_or_stack).cuda()
+        plan = ccl.Plan(*img_or_stack.shape)
+        n = torch.empty(1, dtype=torch.int32, device="cuda")
+    out = torch.empty_like(ref)
+    bad = []
+    for i in range(reps):
+        out.fill_(-7)
+        plan.label(t, out, n)
+        torch.cuda.synchronize()
+        if not torch.equal(n, nref) or not torch.equal(out, ref):
+            bad.append(i)
+    return bad, plan.counters()
+
+
+@pytest.mark.parametrize("case", ["c3_full", "bernoulli06_2048x8192", "handed_over_dense", "c1_batch64"])
+def test_concurrent_union_paths_bit_exact(case):
+    """The tile-local union runs concurrently over all 256 threads of a K1 CTA
+    (shared merge list + per-row leftovers when the list overflows; the
+    full-size pass for long rows).  Each case repeats 200 times, every run
+    bit-exact, and the path counters prove the dense paths ran."""
+    reps = 200
+    if case == "c3_full":
+        bad, c = _stress(synth.generate("c3_percolation_8192"), reps)
+        assert c["k1_merges"] > 0
+    elif case == "bernoulli06_2048x8192":
+        bad, c = _stress(synth.bernoulli(2048, 8192, 0.6, seed=5), reps)
+        assert c["k1_list_overflow"] >= reps, c  # the per-row leftover pass ran on every run
+    elif case == "handed_over_dense":
+        bad, c = _stress(_handed_over_dense(), reps)
+        assert c["k1_handover"] >= reps, c
+        assert c["k1big_list_overflow"] > 0, c
+    else:
+        imgs = [synth.bernoulli(512, 512, 0.5, seed=100 + b) for b in range(64)]
+        bad, c = _stress(imgs, reps, batch=True)
+        assert c["k1_merges"] > 0
+    assert not bad, f"{case}: runs {bad[:10]} of {reps} differ from the oracle ({c})"
+
+
+def test_unaligned_base_pointers():
+    """W % 16 == 0 but img / labels base pointers off 16-byte alignment: the
+    kernels must take the narrow paths (no misaligned vector access)."""
+    H, W = 200, 2048
+    img = synth.bernoulli(H, W, 0.45, seed=9)
+    lo, no = oracle.label(img)
+    for ioff, loff in ((1, 0), (0, 1), (3, 2), (8, 3)):
+        ib = torch.zeros(H * W + 16, dtype=torch.uint8, device="cuda")
+        lb = torch.zeros(H * W + 16, dtype=torch.int32, device="cuda")
+        it = ib[ioff:ioff + H * W].view(H, W)
+        it.copy_(torch.from_numpy(img))
+        out = lb[loff:loff + H * W].view(H, W)
+        n = torch.empty(1, dtype=torch.int32, device="cuda")
+        ccl.label(it, out, n)
+        plan = ccl.Plan(H, W)
+        out2 = torch.zeros_like(out)
+        plan.label(it, out2, n)
+        torch.cuda.synchronize()
+        assert int(n.item()) == no
+        assert np.array_equal(out.cpu().numpy(), lo), (ioff, loff)
+        assert np.array_equal(out2.cpu().numpy(), lo), (ioff, loff)
+
+
+def test_reads_producer_output_on_same_stream():
+    """The kernel right before the call on the stream writes the image: K1
+    must not read a pixel before that kernel completes."""
+    H, W = 4096, 4096
+    a = synth.bernoulli(H, W, 0.45, seed=21)
+    b = synth.bernoulli(H, W, 0.55, seed=22)
+    want = [oracle.label(a), oracle.label(b)]
+    src = [torch.from_numpy(a).cuda().float(), torch.from_numpy(b).cuda().float()]
+    plan = ccl.Plan(H, W)
+    img = torch.empty((H, W), dtype=torch.uint8, device="cuda")
+    out = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    n = torch.empty(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    for i in range(40):
+        k = i % 2
+        torch.gt(src[k] * 3.0, 1.5, out=img.view(torch.bool))  # producer kernel on the current stream
+        plan.label(img, out, n)
+        lo, no = want[k]
+        assert int(n.item()) == no, i
+        assert np.array_equal(out.cpu().numpy(), lo), i
+
+
 @pytest.mark.parametrize("name,h,w", [("c3_percolation_8192", 1024, 2048), ("c4_voronoi_21600", 700, 3000),
                                       ("c2_blobs_1024", 1024, 1024)])
 def test_plans_on_concurrent_streams(name, h, w):
