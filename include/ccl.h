@@ -135,9 +135,24 @@ ccl_status ccl_plan_label(ccl_plan plan, const uint8_t *img, int32_t *labels,
  * device, labels it, copies labels (H*W int32) and N back, and synchronizes
  * `stream` before returning.  Host buffers should be pinned
  * (cudaHostAlloc / torch pin_memory) for full copy bandwidth.  The device
- * staging buffers belong to the plan. */
+ * staging buffers belong to the plan.  = ccl_plan_label_host_async + a
+ * synchronization of `stream`. */
 ccl_status ccl_plan_label_host(ccl_plan plan, const uint8_t *h_img, int32_t *h_labels,
                                int32_t *h_n_components, ccl_stream_t stream);
+
+/* Pipelined end-to-end variant: enqueues the H2D copy, the labeling and the
+ * D2H copy on the plan's own streams (two staging slots), makes `stream`
+ * wait for the D2H, and returns.  The caller synchronizes `stream` (or calls
+ * again) before reading h_labels / *h_n_components, and keeps h_img
+ * unchanged and h_labels / h_n_components untouched until then.  Back-to-back
+ * calls overlap: call i+1's H2D and kernels run while call i's labels are
+ * copied back, so a stream of frames runs at the slower copy direction's
+ * bandwidth.  Ordering: a plan's calls (this one, ccl_plan_label on any
+ * stream) run in call order on its single workspace; the H2D of h_img is not
+ * ordered after earlier work on `stream` (the host buffer must be ready when
+ * the call is made). */
+ccl_status ccl_plan_label_host_async(ccl_plan plan, const uint8_t *h_img, int32_t *h_labels,
+                                     int32_t *h_n_components, ccl_stream_t stream);
 
 /* Per-kernel timing.  ccl_plan_set_profiling(plan, n) arms a ring of n sets
  * of CUDA events (n = 0 disarms): every later ccl_plan_label call records one

@@ -51,6 +51,8 @@ _L.ccl_plan_label.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _L.ccl_plan_label.restype = _i
 _L.ccl_plan_label_host.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _L.ccl_plan_label_host.restype = _i
+_L.ccl_plan_label_host_async.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_L.ccl_plan_label_host_async.restype = _i
 _L.ccl_plan_set_profiling.argtypes = [_vp, _i]
 _L.ccl_plan_set_profiling.restype = _i
 _L.ccl_plan_kernel_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p),
@@ -215,9 +217,7 @@ class Plan:
                                  _stream_handle(stream)), "ccl_plan_label")
         return out, n_out
 
-    def label_host(self, img, out, n_out, stream=None):
-        """End to end with HOST (ideally pinned) tensors: H2D copy, label, D2H
-        copy, stream synchronize -- all inside the library."""
+    def _check_host(self, img, out, n_out):
         for t, dt in ((img, torch.uint8), (out, torch.int32), (n_out, torch.int32)):
             if t.is_cuda or t.dtype != dt or not t.is_contiguous():
                 raise TypeError("label_host takes contiguous host tensors (uint8 img, int32 out/n)")
@@ -225,8 +225,23 @@ class Plan:
         nb = 1 if self.B is None else self.B
         if tuple(img.shape) != shape or tuple(out.shape) != shape or n_out.numel() < nb:
             raise ValueError(f"plan is for {shape} (n_out >= {nb} elements)")
+
+    def label_host(self, img, out, n_out, stream=None):
+        """End to end with HOST (ideally pinned) tensors: H2D copy, label, D2H
+        copy, stream synchronize -- all inside the library."""
+        self._check_host(img, out, n_out)
         _check(_L.ccl_plan_label_host(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
                                       _stream_handle(stream)), "ccl_plan_label_host")
+        return out, n_out
+
+    def label_host_async(self, img, out, n_out, stream=None):
+        """Pipelined end to end (ccl_plan_label_host_async): returns at once;
+        synchronize `stream` before reading out / n_out.  Back-to-back calls
+        overlap one call's H2D and kernels with the previous call's D2H.  Keep
+        img / out / n_out alive and untouched until then."""
+        self._check_host(img, out, n_out)
+        _check(_L.ccl_plan_label_host_async(self._p, img.data_ptr(), out.data_ptr(), n_out.data_ptr(),
+                                            _stream_handle(stream)), "ccl_plan_label_host_async")
         return out, n_out
 
     def set_profiling(self, nsets=1):

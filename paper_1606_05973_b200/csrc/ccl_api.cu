@@ -120,9 +120,21 @@ struct ccl_plan_st {
     void *ws_mem = nullptr;
     size_t ws_bytes = 0;
     Workspace ws;
-    uint8_t *d_img = nullptr;   // staging buffers for ccl_plan_label_host
-    int32_t *d_lab = nullptr;
-    int32_t *d_n = nullptr;
+    // ccl_plan_label_host_async: two staging slots, three internal streams
+    // (H2D, compute, D2H) and per-slot events, so step i+1's H2D and kernels
+    // overlap step i's D2H
+    bool host_init = false;
+    cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_cmp[2] = {}, ev_d2h[2] = {};
+    uint8_t *a_img[2] = {};
+    int32_t *a_lab[2] = {}, *a_n[2] = {};
+    int slot = 0;
+    // ordering of the plan's pipelines across the async host path and the
+    // device path (one workspace): the stream of the last device-path call,
+    // and an event after it once the host pipe exists
+    cudaStream_t last_dev_stream = nullptr;
+    bool dev_called = false, dev_pending = false;
+    cudaEvent_t ev_dev = nullptr;
     int prof_sets = 0;             // profiling ring size (0 = off)
     cudaEvent_t *ev = nullptr;     // prof_sets * (K_COUNT + 1) events
     long long prof_calls = 0;      // profiled calls since the ring was (re)armed
@@ -244,13 +256,51 @@ ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out) {
     return CCL_OK;
 }
 
+static void free_host_pipe(ccl_plan p) {
+    if (!p->host_init) return;
+    for (cudaStream_t s : {p->s_h2d, p->s_cmp, p->s_d2h})
+        if (s) cudaStreamSynchronize(s);
+    for (int k = 0; k < 2; k++) {
+        for (cudaEvent_t e : {p->ev_h2d[k], p->ev_cmp[k], p->ev_d2h[k]})
+            if (e) cudaEventDestroy(e);
+        if (p->a_img[k]) cudaFree(p->a_img[k]);
+        if (p->a_lab[k]) cudaFree(p->a_lab[k]);
+        if (p->a_n[k]) cudaFree(p->a_n[k]);
+    }
+    for (cudaStream_t s : {p->s_h2d, p->s_cmp, p->s_d2h})
+        if (s) cudaStreamDestroy(s);
+    if (p->ev_dev) cudaEventDestroy(p->ev_dev);
+    p->host_init = false;
+}
+
+static cudaError_t init_host_pipe(ccl_plan p) {
+    if (p->host_init) return cudaSuccess;
+    p->host_init = true;  // (free_host_pipe releases whatever was made)
+    const size_t n = (size_t)p->g.H * (size_t)p->g.W;
+    const size_t nn = sizeof(int32_t) * (size_t)(p->g.nTy / p->g.tpi);
+    cudaError_t e;
+    for (cudaStream_t *s : {&p->s_h2d, &p->s_cmp, &p->s_d2h})
+        if ((e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p->ev_dev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if (p->dev_called) {  // device-path calls made before the pipe existed
+        if ((e = cudaEventRecord(p->ev_dev, p->last_dev_stream)) != cudaSuccess) return e;
+        p->dev_pending = true;
+    }
+    for (int k = 0; k < 2; k++) {
+        for (cudaEvent_t *ev : {&p->ev_h2d[k], &p->ev_cmp[k], &p->ev_d2h[k]})
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&p->a_img[k], n)) != cudaSuccess || (e = cudaMalloc(&p->a_lab[k], n * 4)) != cudaSuccess ||
+            (e = cudaMalloc(&p->a_n[k], nn)) != cudaSuccess)
+            return e;
+    }
+    return cudaSuccess;
+}
+
 ccl_status ccl_plan_destroy(ccl_plan p) {
     if (!p) return CCL_INVALID_ARGUMENT;
+    free_host_pipe(p);
     cudaError_t e = cudaSuccess;
     if (p->ws_mem) e = cudaFree(p->ws_mem);
-    if (p->d_img) cudaFree(p->d_img);
-    if (p->d_lab) cudaFree(p->d_lab);
-    if (p->d_n) cudaFree(p->d_n);
     free_events(p);
     delete p;
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
@@ -279,31 +329,70 @@ ccl_status ccl_plan_label(ccl_plan p, const uint8_t *img, int32_t *labels, int32
         ev = p->ev + (p->prof_calls % p->prof_sets) * (K_COUNT + 1);
         p->prof_calls++;
     }
-    cudaError_t e = run_pipeline(p->g, p->ws, img, labels, n_components, s, ev);
+    cudaError_t e = cudaSuccess;
+    if (p->host_init) {  // after the async host path's last kernels (same workspace)
+        e = cudaStreamWaitEvent(s, p->ev_cmp[p->slot ^ 1], 0);
+    }
+    if (e == cudaSuccess) e = run_pipeline(p->g, p->ws, img, labels, n_components, s, ev);
+    if (e == cudaSuccess && p->host_init) {
+        e = cudaEventRecord(p->ev_dev, s);
+        p->dev_pending = true;
+    }
+    p->dev_called = true;
+    p->last_dev_stream = s;
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+}
+
+ccl_status ccl_plan_label_host_async(ccl_plan p, const uint8_t *h_img, int32_t *h_labels,
+                                     int32_t *h_n_components, ccl_stream_t stream) {
+    if (!p || !h_img || !h_labels || !h_n_components) return CCL_INVALID_ARGUMENT;
+    const size_t n = (size_t)p->g.H * (size_t)p->g.W;
+    const size_t nn = sizeof(int32_t) * (size_t)(p->g.nTy / p->g.tpi);
+    cudaError_t e = init_host_pipe(p);
+    if (e != cudaSuccess) {
+        free_host_pipe(p);
+        return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
+    }
+    const int k = p->slot;
+    p->slot ^= 1;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+#define CKA(x)                                   \
+    do {                                         \
+        if ((x) != cudaSuccess) return CCL_CUDA_ERROR; \
+    } while (0)
+    // H2D into slot k once the kernels of the call before last are done with it
+    CKA(cudaStreamWaitEvent(p->s_h2d, p->ev_cmp[k], 0));
+    CKA(cudaMemcpyAsync(p->a_img[k], h_img, n, cudaMemcpyHostToDevice, p->s_h2d));
+    CKA(cudaEventRecord(p->ev_h2d[k], p->s_h2d));
+    // kernels: after this call's H2D and after the D2H that last read slot k
+    CKA(cudaStreamWaitEvent(p->s_cmp, p->ev_h2d[k], 0));
+    CKA(cudaStreamWaitEvent(p->s_cmp, p->ev_d2h[k], 0));
+    if (p->dev_pending) {  // a device-path call since the last async call
+        CKA(cudaStreamWaitEvent(p->s_cmp, p->ev_dev, 0));
+        p->dev_pending = false;
+    }
+    cudaEvent_t *ev = nullptr;
+    if (p->prof_sets > 0) {
+        ev = p->ev + (p->prof_calls % p->prof_sets) * (K_COUNT + 1);
+        p->prof_calls++;
+    }
+    CKA(run_pipeline(p->g, p->ws, p->a_img[k], p->a_lab[k], p->a_n[k], p->s_cmp, ev));
+    CKA(cudaEventRecord(p->ev_cmp[k], p->s_cmp));
+    // D2H of the labels and N, then the caller's stream waits for it
+    CKA(cudaStreamWaitEvent(p->s_d2h, p->ev_cmp[k], 0));
+    CKA(cudaMemcpyAsync(h_labels, p->a_lab[k], n * 4, cudaMemcpyDeviceToHost, p->s_d2h));
+    CKA(cudaMemcpyAsync(h_n_components, p->a_n[k], nn, cudaMemcpyDeviceToHost, p->s_d2h));
+    CKA(cudaEventRecord(p->ev_d2h[k], p->s_d2h));
+    CKA(cudaStreamWaitEvent(s, p->ev_d2h[k], 0));
+#undef CKA
+    return CCL_OK;
 }
 
 ccl_status ccl_plan_label_host(ccl_plan p, const uint8_t *h_img, int32_t *h_labels,
                                int32_t *h_n_components, ccl_stream_t stream) {
-    if (!p || !h_img || !h_labels || !h_n_components) return CCL_INVALID_ARGUMENT;
-    const size_t n = (size_t)p->g.H * (size_t)p->g.W;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    cudaError_t e;
-    if (!p->d_img) {
-        if ((e = cudaMalloc(&p->d_img, n)) != cudaSuccess ||
-            (e = cudaMalloc(&p->d_lab, n * 4)) != cudaSuccess ||
-            (e = cudaMalloc(&p->d_n, sizeof(int32_t) * (p->g.nTy / p->g.tpi))) != cudaSuccess)
-            return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
-    }
-    if (cudaMemcpyAsync(p->d_img, h_img, n, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return CCL_CUDA_ERROR;
-    ccl_status st = ccl_plan_label(p, p->d_img, p->d_lab, p->d_n, stream);
+    ccl_status st = ccl_plan_label_host_async(p, h_img, h_labels, h_n_components, stream);
     if (st != CCL_OK) return st;
-    if (cudaMemcpyAsync(h_labels, p->d_lab, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(h_n_components, p->d_n, sizeof(int32_t) * (p->g.nTy / p->g.tpi), cudaMemcpyDeviceToHost,
-                        s) != cudaSuccess)
-        return CCL_CUDA_ERROR;
-    return cudaStreamSynchronize(s) == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
+    return cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;
 }
 
 ccl_status ccl_plan_set_profiling(ccl_plan p, int nsets) {

@@ -194,6 +194,36 @@ def test_label_host_end_to_end():
     assert int(h_n[0]) == no and np.array_equal(h_lab.numpy(), lo)
 
 
+def test_label_host_async_pipelined_frames():
+    """ccl_plan_label_host_async: a stream of different frames back to back
+    (two staging slots, each call's H2D/kernels overlapping the previous
+    D2H), mixed with device-path calls on the same plan and another stream;
+    every frame's host labels bit-exact."""
+    H, W = 1500, 2600
+    frames = [synth.scaled("c4_voronoi_21600", H, W), synth.bernoulli(H, W, 0.45, seed=3),
+              synth.scaled("c3_percolation_8192", H, W), synth.bernoulli(H, W, 0.6, seed=4)]
+    want = [oracle.label(f) for f in frames]
+    plan = ccl.Plan(H, W)
+    h_imgs = [torch.from_numpy(f).pin_memory() for f in frames]
+    outs = [torch.empty((H, W), dtype=torch.int32).pin_memory() for _ in range(8)]
+    ns = [torch.empty(1, dtype=torch.int32).pin_memory() for _ in range(8)]
+    side = torch.cuda.Stream()
+    d_img = torch.from_numpy(frames[1]).cuda()
+    d_out = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    d_n = torch.empty(1, dtype=torch.int32, device="cuda")
+    for i in range(8):
+        plan.label_host_async(h_imgs[i % 4], outs[i], ns[i])
+        if i == 3:
+            with torch.cuda.stream(side):
+                plan.label(d_img, d_out, d_n, stream=side)
+    torch.cuda.synchronize()
+    for i in range(8):
+        lo, no = want[i % 4]
+        assert int(ns[i][0]) == no and np.array_equal(outs[i].numpy(), lo), i
+    lo, no = want[1]
+    assert int(d_n.item()) == no and np.array_equal(d_out.cpu().numpy(), lo)
+
+
 def test_kernel_times_profiling():
     img = torch.from_numpy(synth.bernoulli(640, 2048, 0.5, 3)).cuda()
     plan = ccl.Plan(640, 2048)
