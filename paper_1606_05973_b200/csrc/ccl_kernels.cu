@@ -236,7 +236,29 @@ __device__ __forceinline__ int gfind_ro(const int32_t *par, int x) {
         x = px;
     }
 }
+// Find with path halving on a forest that may hang under foreign roots (row
+// bands: a parent -2-f is a root owned by another band, terminal).  Used
+// after the unions (K4): only non-roots are rewritten, each to an ancestor
+// (possibly the foreign reference), so roots and the partition are unchanged;
+// concurrent finds shorten each other's chains (C5b comb: chains of 512 tile
+// rows).
+__device__ __forceinline__ int gfind_halve(int32_t *par, int x) {
+    while (true) {
+        const int px = __ldcg(par + x);
+        if (px == x || px < 0) return px;
+        const int ppx = __ldcg(par + px);
+        if (ppx == px) return px;
+        __stcg(par + x, ppx);
+        if (ppx < 0) return ppx;
+        x = ppx;
+    }
+}
 // Links the root with the larger key under the root with the smaller key.
+// Links the root with the larger key under the root with the smaller key
+// (merger's lock + "still a root?" re-check, as a CAS).
+// (Rem's interleaved climb without the splice, linking a root under the
+// other side's parent, was measured too: C4 K2 37 -> 91 us, C5b 0.7 -> 5.3
+// ms -- two key loads per step and no compression on the long chains.)
 __device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
     while (true) {
         a = gfind(par, a);
@@ -824,7 +846,6 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     __shared__ uint32_t shd[K2_WARPS][2][WPR], sbs[K2_WARPS][2][WPR];
     constexpr int PCAP = 128;
     __shared__ uint32_t plist[K2_WARPS][PCAP];  // the edge's unions: (upper run, lower run) ordinals
-    __shared__ int pcnt[K2_WARPS];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * K2_WARPS + wib;
     if (gw < nh_warps) {
@@ -839,24 +860,14 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
         __syncwarp();
         const int32_t *bot = ws.botnode + (int64_t)((ty - 1) * g.nTx + tx) * g.maxrun;
         const int32_t *top = ws.topnode + (int64_t)(ty * g.nTx + tx) * g.maxrun;
-        if (lane == 0) pcnt[wib] = 0;
-        __syncwarp();
         // the edge's unions are listed first (run ordinals, shared memory
         // only) and then done one per lane: a lane with several edges no
-        // longer runs their global union chains one after another
-        auto add = [&](int ou, int ox) {
-            const int i = atomicAdd(&pcnt[wib], 1);
-            if (i < PCAP) plist[wib][i] = (uint32_t)ou | ((uint32_t)ox << 16);
-            else gunion(ws.gparent, ws.gkey, bot[ou], top[ox]);  // list full
-        };
-        uint32_t m = first_in_run(x & dilate(U), x);
-        while (m) {
-            int b = __ffs(m) - 1;
-            m &= m - 1;
-            int q = 32 * lane + b + leftmost3(u, U.xp, U.xn, b);
-            int lq = q >> 5;
-            add(run_ord(shd[wib][0][lq], sbs[wib][0][lq], q & 31), run_ord(X.hx, X.base, b));
-        }
+        // longer runs their global union chains one after another.  Every
+        // lane's edges get consecutive list positions (a warp scan of its
+        // counts); a dense edge (more than PCAP unions) is worked through in
+        // windows of PCAP, each fully lane-parallel.
+        const uint32_t m1 = first_in_run(x & dilate(U), x);
+        uint32_t m2;
         // upper runs whose leftmost lower neighbour has another leftmost upper
         // neighbour (see upper_merge_heads in K1)
         {
@@ -865,20 +876,33 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
             const uint32_t S_ = s | (cin ? (x & ~(x + 1)) : 0u);
             // (no hole-bridged filter: it only drops redundant edges)
-            m = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_);
+            m2 = upper_merge_heads(U.hx, u, U.xp, x, X.xp, S_);
         }
-        while (m) {
-            int b = __ffs(m) - 1;
-            m &= m - 1;
-            int q = 32 * lane + b - 1;  // lower pixel h-1
-            int lq = q >> 5;
-            add(run_ord(U.hx, U.base, b), run_ord(shd[wib][1][lq], sbs[wib][1][lq], q & 31));
-        }
-        __syncwarp();
-        const int np = min(pcnt[wib], PCAP);
-        for (int i = lane; i < np; i += 32) {
-            const uint32_t e = plist[wib][i];
-            gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
+        uint32_t tot;
+        const int base = (int)warp_excl_scan(__popc(m1) + __popc(m2), tot);
+        for (int w0 = 0; w0 < (int)tot; w0 += PCAP) {
+            int idx = base - w0;  // this lane's next entry, relative to the window
+            for (uint32_t m = m1; m && idx < PCAP; m &= m - 1, idx++) {
+                if (idx < 0) continue;
+                const int b = __ffs(m) - 1;
+                const int q = 32 * lane + b + leftmost3(u, U.xp, U.xn, b), lq = q >> 5;
+                plist[wib][idx] = (uint32_t)run_ord(shd[wib][0][lq], sbs[wib][0][lq], q & 31) |
+                                  ((uint32_t)run_ord(X.hx, X.base, b) << 16);
+            }
+            for (uint32_t m = m2; m && idx < PCAP; m &= m - 1, idx++) {
+                if (idx < 0) continue;
+                const int b = __ffs(m) - 1;
+                const int q = 32 * lane + b - 1, lq = q >> 5;  // lower pixel h-1
+                plist[wib][idx] = (uint32_t)run_ord(U.hx, U.base, b) |
+                                  ((uint32_t)run_ord(shd[wib][1][lq], sbs[wib][1][lq], q & 31) << 16);
+            }
+            __syncwarp();
+            const int np = min(PCAP, (int)tot - w0);
+            for (int i = lane; i < np; i += 32) {
+                const uint32_t e = plist[wib][i];
+                gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
+            }
+            __syncwarp();
         }
         return;
     }
@@ -1232,14 +1256,14 @@ k_fixup(Geometry g, Workspace ws) {
 #pragma unroll
     for (int t = 0; t < 4; t++) {
         if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
-        const int r = par[t] < 0 ? par[t] : gfind_ro(ws.gparent, par[t]);
+        const int r = par[t] < 0 ? par[t] : gfind_halve(ws.gparent, par[t]);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
         st_keep(complab + (gcv[t] & 0xFFFF), lab, keep);
     }
     for (int j = lane + 128; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) == node) continue;
-        const int r = gfind_ro(ws.gparent, node);
+        const int r = gfind_halve(ws.gparent, node);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
         st_keep(complab + (__ldcg(ws.gnodecomp + node) & 0xFFFF), lab, keep);
     }
