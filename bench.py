@@ -389,7 +389,7 @@ def main():
         step = lambda: plan.label(d_img, out, n_out)  # noqa: E731
         nTx, nTy = (W + 1023) // 1024, (H + 31) // 32
         # mirrors cclb::pipeline_launches: k_border only runs when tiles have neighbours
-        launches_per_step = 6 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
+        launches_per_step = 5 + (1 if (nTy - 1) * nTx + (nTx - 1) * H > 0 else 0)
     else:
         with stdout_to_stderr():
             uid = ccl.nccl_unique_id() if rank == 0 else None
@@ -402,9 +402,9 @@ def main():
         plan = None
         # our kernels per band step (ccl_bands.cu): K1 (+ its hand-over pass), K2, boundary rows,
         # 2 slot representatives (the second also starts the slot union-find),
-        # slot unions, link, K3, K3b, export (+ band offset), K4, K5 (the 3
-        # NCCL all-gathers are not counted)
-        launches_per_step = 13
+        # slot unions, link, K3, export (+ band offset), K4, K5 (the 3 NCCL
+        # all-gathers are not counted)
+        launches_per_step = 12
 
     for _ in range(max(3, args.warmup)):
         step()

@@ -29,6 +29,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
     g.maxrun = (tw + 1) / 2;
     g.capc = ((th + 1) / 2) * g.maxrun;
     g.capb = 2 * g.maxrun + th;
+    g.capw = (g.capc + 31) / 32;
     g.aligned = (W % 16) == 0;
     g.row0 = 0;
     g.thr = 0;
@@ -36,7 +37,7 @@ Geometry make_geometry_batch(int B, int IH, int W) {
 }
 
 enum {
-    A_BM, A_RUNCOMP, A_COMPNODE, A_COMPLAB, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
+    A_BM, A_RUNCOMP, A_COMPNODE, A_NRLAB, A_TLB, A_TBITS, A_TWPRE, A_GPARENT, A_GKEY, A_GNODECOMP, A_GNODELAB,
     A_EDGEROW, A_TOP, A_BOT, A_LEFT, A_RIGHT, A_META, A_SEGCNT, A_SEGOFF, A_SCANSTATE, A_TICKET, A_ROWEXCL, A_K1OVER, A_STATS, A_COUNT
 };
 
@@ -46,7 +47,10 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total) {
         H * g.WW * 4,                   // bm
         H * g.nTx * g.maxrun * 2,       // runcomp
         nT * g.capc * 4,                // compnode
-        nT * g.capc * 4,                // complab
+        nT * g.capc * 4,                // nrlab
+        nT * TH * 4,                    // tlb
+        nT * g.capw * 4,                // tbits
+        nT * g.capw * 4,                // twpre
         nT * g.capb * 4,                // gparent
         nT * g.capb * 8,                // gkey
         nT * g.capb * 4,                // gnodecomp
@@ -81,7 +85,10 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     w.bm = reinterpret_cast<uint32_t *>(b + offs[A_BM]);
     w.runcomp = reinterpret_cast<uint16_t *>(b + offs[A_RUNCOMP]);
     w.compnode = reinterpret_cast<int32_t *>(b + offs[A_COMPNODE]);
-    w.complab = reinterpret_cast<int32_t *>(b + offs[A_COMPLAB]);
+    w.nrlab = reinterpret_cast<int32_t *>(b + offs[A_NRLAB]);
+    w.tlb = reinterpret_cast<int32_t *>(b + offs[A_TLB]);
+    w.tbits = reinterpret_cast<uint32_t *>(b + offs[A_TBITS]);
+    w.twpre = reinterpret_cast<int32_t *>(b + offs[A_TWPRE]);
     w.gparent = reinterpret_cast<int32_t *>(b + offs[A_GPARENT]);
     w.gkey = reinterpret_cast<int64_t *>(b + offs[A_GKEY]);
     w.gnodecomp = reinterpret_cast<int32_t *>(b + offs[A_GNODECOMP]);

@@ -186,11 +186,11 @@ ccl_status xband_init(XBand &x, int nb, int W) {
 // A: local labeling; slot keys / nodes / representatives into (keys, reps)
 // Profiling events of a band step (ShardPlan profiling), SHARD_EV per set:
 // 0 K1, 1 K2, 2 cross-band exchange (row roots, representatives,
-// all-gather, slot unions, links), 3 K3, 4 K3b, 5 count all-gather + export
-// + label all-gather, 6 K4, 7 K5, 8 end.
-constexpr int SHARD_EV = 9;
+// all-gather, slot unions, links), 3 K3, 4 count all-gather + export +
+// label all-gather, 5 K4, 6 K5, 7 end.
+constexpr int SHARD_EV = 8;
 const char *const kShardNames[SHARD_EV - 1] = {"k_tile_local", "k_border", "xband_exchange", "k_number",
-                                                "k_label", "xband_export", "k_fixup", "k_write"};
+                                                "xband_export", "k_fixup", "k_write"};
 
 ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *reps, int32_t *spar, int spar_lo,
                         int spar_hi, cudaStream_t s, cudaEvent_t *ev = nullptr) {
@@ -207,7 +207,7 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
 ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s,
                          cudaEvent_t *ev = nullptr) {
     CK(band_link(b.ws, x.W, self, x.keys, x.spar, b.d_nodes, s));
-    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 1 : nullptr));  // ev[3], ev[4]
+    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 1 : nullptr));  // ev[3]
     return CCL_OK;
 }
 
@@ -221,7 +221,7 @@ ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int
 // E: labels of merged components (foreign ones from the exported table) + write
 ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s, cudaEvent_t *ev = nullptr) {
     b.ws.xlab = x.exps;
-    CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 2 : nullptr));  // ev[6], ev[7], ev[8]
+    CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 2 : nullptr));  // ev[5], ev[6], ev[7]
     return CCL_OK;
 }
 
@@ -397,7 +397,7 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     // B + C + X2
     CK(band_resolve(p->nranks, p->W, x.keys, x.reps, x.spar, s));
     if ((st = band_phase_bc(b, x, self, x.counts + self, s, ev)) != CCL_OK) return st;
-    if (ev) CK(cudaEventRecord(ev[5], s));
+    if (ev) CK(cudaEventRecord(ev[4], s));
     CKN(ncclAllGather(x.counts + self, x.counts, 1, ncclInt32, p->comm, s));
     // D + X3
     if ((st = band_phase_d(b, x, self, n_components, x.exps + self * slots, s)) != CCL_OK) return st;

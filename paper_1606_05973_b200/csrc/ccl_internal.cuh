@@ -34,6 +34,7 @@ struct Geometry {
     int maxrun;    // runs per tile row bound: ceil(min(W,TW)/2)
     int capc;      // components per tile bound: ceil(min(H,TH)/2) * maxrun
     int capb;      // border components per tile bound: 2*maxrun + min(H,TH)
+    int capw;      // words of a tile's component bitmap: ceil(capc/32)
     int aligned;   // W % 16 == 0: 16-byte vector loads / stores are legal
     int IH;        // rows per image: a batch is B images of IH x W stacked in memory (H = B*IH)
     int tpi;       // tile rows per image = ceil(IH/TH); tile rows never straddle two images
@@ -44,9 +45,15 @@ struct Geometry {
 // Device workspace (all arrays carved from one allocation; see ccl_api.cu).
 struct Workspace {
     uint32_t *bm;         // [H][WW]           foreground bitmask, bit i of word k = column 32k+i
-    uint16_t *runcomp;    // [H][nTx][maxrun]  tile component of each run of each tile row
+    uint16_t *runcomp;    // [H][nTx][maxrun]  (root row << 9) | root rank in its row, of each run
+                          //                   (tile component = rowfirst[root row] + rank)
     int32_t *compnode;    // [nT][capc]        border-node id of a border component (others unset)
-    int32_t *complab;     // [nT][capc]        band-local label of the component (1..N_band)
+    int32_t *nrlab;       // [nT][capc]        band-local label of the j-th non-root border component
+                          //                   of the tile (j = non-roots before it, K4)
+    int32_t *tlb;         // [nT][TH]          label base of each tile row r: label of a root
+                          //                   component = tlb[r] + rank - (non-roots before it)
+    uint32_t *tbits;      // [nT][capw]        bitmap of the tile's non-root border components
+    int32_t *twpre;       // [nT][capw]        exclusive popcount prefix of tbits
     int32_t *gparent;     // [nT][capb]        global union-find over border components
     int64_t *gkey;        // [nT][capb]        (image row, tile column, run ordinal) key: raster order
     int32_t *gnodecomp;   // [nT][capb]        (root row in tile << 16) | tile component of the node
@@ -106,7 +113,7 @@ enum {
     STAT_COUNT
 };
 
-enum { K_TILE = 0, K_BORDER, K_NUMBER, K_LABEL, K_FIXUP, K_WRITE, K_COUNT };
+enum { K_TILE = 0, K_BORDER, K_NUMBER, K_FIXUP, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 
 // Enqueues the whole single-GPU pipeline on `stream`.  If `ev` is non-null it

@@ -35,8 +35,7 @@ namespace cclb {
 
 #define FULL 0xFFFFFFFFu
 
-const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number", "k_label",
-                                           "k_fixup", "k_write"};
+const char *const kKernelNames[K_COUNT] = {"k_tile_local", "k_border", "k_number", "k_fixup", "k_write"};
 
 // ===================================================================== helpers
 // Programmatic dependent launch: a kernel waits for its predecessor's grid to
@@ -755,7 +754,9 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
             const int c = __shfl_sync(FULL, rowfirst, r / MR) + (int)(pr & 0x1FFu);
             if (o < n) {
-                dst[o] = (uint16_t)c;
+                // runcomp = (root row << 9) | rank of the root in its row; the
+                // component is rowfirst[row] + rank (K5 needs the row)
+                dst[o] = (uint16_t)(((uint32_t)(r / MR) << 9) | (pr & 0x1FFu));
             }
             if (hasb) {
                 // node number of the chunk's first border root, for P4c
@@ -951,10 +952,19 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
 // [rowfirst[r], rowfirst[r+1]) minus the few border components that are not
 // roots.  The root counts of the tile row's segments (row, tile column) are
 // scanned in raster order, chained across tile rows with a decoupled
-// lookback, and every root gets  offset(segment) + rank in segment + 1:
-// flatten's consecutive numbering k++  made canonical.
+// lookback: flatten's consecutive numbering k++  made
+// canonical.  Per tile (one warp) the kernel leaves what K4 and K5 need to
+// label any component c = rowfirst[row] + rank of the tile:
+//   tbits / twpre  bitmap of the non-root border components + its popcount
+//                  prefix (nonroots_before(c) = twpre[c/32] + popc(...));
+//   tlb[row]       excl(tile row) + segoff(row, tile) + non-roots in earlier
+//                  rows + 1, so a root's label = tlb[row] + rank -
+//                  nonroots_before(c);
+//   gnodelab       the labels of the tile's root border nodes (K4 reads them
+//                  for the components merged into them).
 struct KNSmem {
     int32_t nrrow[KN_WARPS][TH];           // non-root border components per row
+    uint32_t bits[KN_WARPS][CAPC / 32];    // the warp's tile's non-root bitmap
     int32_t wsum[KN_WARPS];
     int32_t part, excl;
 };
@@ -971,7 +981,8 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     const int ty = sm.part;
     const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
     const bool first = ty % g.tpi == 0;  // first tile row of its image: numbering starts at 1
-    // ---- phase 1: root counts of the segments (R0 + r, tx)
+    // ---- phase 1: non-root border components of every tile (bitmap, prefix,
+    // counts per row) and the root counts of the segments (R0 + r, tx)
     for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
         const int tile = ty * g.nTx + tx;
         const int32_t *meta = ws.meta + (int64_t)tile * META;
@@ -989,19 +1000,47 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
             par[t] = j < g.capb ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
             gcv[t] = j < g.capb ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
         }
+        const int nbw = (ncomp + 31) >> 5;
         int32_t *nrrow = sm.nrrow[w];
+        uint32_t *bits = sm.bits[w];
         nrrow[lane] = 0;
+        for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < 4; t++)
-            if (lane + 32 * t < nborder && par[t] != nodebase + lane + 32 * t) atomicAdd(nrrow + (gcv[t] >> 16), 1);
+            if (lane + 32 * t < nborder && par[t] != nodebase + lane + 32 * t) {
+                const int c = gcv[t] & 0xFFFF;
+                atomicOr(bits + (c >> 5), 1u << (c & 31));
+                atomicAdd(nrrow + (gcv[t] >> 16), 1);
+            }
         for (int j = lane + 128; j < nborder; j += 32) {
             const int node = nodebase + j;
-            if (__ldcg(ws.gparent + node) != node) atomicAdd(nrrow + (__ldcg(ws.gnodecomp + node) >> 16), 1);
+            if (__ldcg(ws.gparent + node) != node) {
+                const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
+                atomicOr(bits + (c >> 5), 1u << (c & 31));
+                atomicAdd(nrrow + (gc >> 16), 1);
+            }
         }
         __syncwarp();
         const int rfn = lane + 1 < rows ? rfx : ncomp;
         if (lane < rows) ws.segcnt[(int64_t)(R0 + lane) * g.nTx + tx] = rfn - rf - nrrow[lane];
+        // the bitmap and its popcount prefix (K4, K5); the non-roots of the
+        // earlier rows (lane = row) wait in tlb for phase 3
+        uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+        int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+        for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
+            const int j = j0 + lane;
+            const uint32_t b = j < nbw ? bits[j] : 0u;
+            uint32_t tot;
+            const int pre = (int)warp_excl_scan(__popc(b), tot);
+            if (j < nbw) {
+                tbits[j] = b;
+                twpre[j] = acc + pre;
+            }
+            acc += (int)tot;
+        }
+        uint32_t tot;
+        ws.tlb[(int64_t)tile * TH + lane] = (int)warp_excl_scan((uint32_t)nrrow[lane], tot);
         __syncwarp();
     }
     __syncthreads();
@@ -1072,157 +1111,35 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) ws.rowexcl[ty] = sm.excl;
-}
-
-// ======================================================================== K3b
-// One warp per tile: labels of the tile's global roots (components and
-// border nodes):  offset(segment) + rank in segment + 1, where the rank of a
-// root among the roots of its segment is its component index minus the
-// components of earlier rows minus the non-root border components before it.
-constexpr int KL_WARPS = 2;  // small CTAs: finer scheduling of the 1-2 waves (measured vs 4, 8, 16)
-struct KLSmem {
-    uint32_t nrbits[KL_WARPS][CAPC / 32];  // non-root border components of the warp's tile
-    uint16_t wpre[KL_WARPS][CAPC / 32];    // exclusive popcount prefix of nrbits
-    int32_t nrrow[KL_WARPS][TH];           // non-roots per row
-    int32_t rbase[KL_WARPS][TH];           // label of the row's first root minus its index
-};
-
-#ifndef KL_TPW
-#define KL_TPW 1  // tiles per warp (grid-stride)
-#endif
-__device__ __forceinline__ void label_tile(const Geometry &g, const Workspace &ws, KLSmem &sm, int tile, int w,
-                                           int lane) {
-    const int tx = tile % g.nTx, ty = tile / g.nTx;
-    const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
-    const int32_t *meta = ws.meta + (int64_t)tile * META;
-    const int ncomp = __ldcg(meta + META_NCOMP), nborder = __ldcg(meta + META_NBORDER);
-    const int f = __ldcg(meta + META_ROWFIRST + lane);
-    const int so = lane < rows ? __ldcg(ws.segoff + (int64_t)(R0 + lane) * g.nTx + tx) : 0;
-    const int excl = __ldcg(ws.rowexcl + ty);
-    const int nbw = (ncomp + 31) >> 5;
-    uint32_t *bits = sm.nrbits[w];
-    uint16_t *wpre = sm.wpre[w];
-    int32_t *rb = sm.rbase[w];
-    int32_t *nrrow = sm.nrrow[w];
-    const int nodebase = tile * g.capb;
-    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-    const uint64_t keep = pol_evict_last();  // component labels stay in L2 for K5
-    // every independent load of the tile at once: the parent and (row,
-    // component) of up to KL_NODES border nodes per lane and the root rows
-    // of the first 4*32 components
-    constexpr int KL_NODES = 4;
-    int par[KL_NODES], gcv[KL_NODES];
-#pragma unroll
-    for (int t = 0; t < KL_NODES; t++) {  // inside the tile's capb slots: no wait for nborder
-        const int j = lane + 32 * t;
-        par[t] = j < g.capb ? __ldcg(ws.gparent + nodebase + j) : 0;
-        gcv[t] = j < g.capb ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
-    }
-    // non-root border components (bits) and their count per row
-    for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
-    nrrow[lane] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < KL_NODES; t++) {
-        const int j = lane + 32 * t;
-        if (j < nborder && par[t] != nodebase + j) {
-            const int c = gcv[t] & 0xFFFF;
-            atomicOr(bits + (c >> 5), 1u << (c & 31));
-            atomicAdd(nrrow + (gcv[t] >> 16), 1);
-        }
-    }
-    for (int j = lane + 32 * KL_NODES; j < nborder; j += 32) {
-        const int node = nodebase + j;
-        if (__ldcg(ws.gparent + node) != node) {
-            const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
-            atomicOr(bits + (c >> 5), 1u << (c & 31));
-            atomicAdd(nrrow + (gc >> 16), 1);
-        }
-    }
-    __syncwarp();
-    for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
-        const int j = j0 + lane;
-        const uint32_t pc = j < nbw ? __popc(bits[j]) : 0u;
-        uint32_t tot;
-        const int pre = (int)warp_excl_scan(pc, tot);
-        if (j < nbw) wpre[j] = (uint16_t)(acc + pre);
-        acc += (int)tot;
-    }
-    {
-        uint32_t tot;
-        const int nrp = (int)warp_excl_scan((uint32_t)nrrow[lane], tot);
-        // label(c) = excl + segoff + (roots before c in the tile) - (roots
-        // in earlier rows) + 1, roots before c = c - nonroots before c
-        rb[lane] = excl + so - (f - nrp) + 1;
-    }
-    __syncwarp();
-    auto nonroots_before = [&](int c) -> int {
-        return wpre[c >> 5] + __popc(bits[c >> 5] & ((1u << (c & 31)) - 1u));
-    };
-    {
-        // the root row of component c: the last row whose first component is
-        // <= c (the tile's row offsets in shared memory)
-        // Each group of 32 consecutive components (one per lane) sees the
-        // few rows that start inside it through a warp-uniform walk over the
-        // row offsets held by the lanes (lane r = row r): no divergence, no
-        // memory.  rcur = last row starting at or before the group.
-        int rcur = 0;
-        for (int gb = 0; gb < ncomp; gb += 128) {  // warp-uniform trip count (shuffles inside)
-            const int c0 = gb + lane;
-            int rr4[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int base = gb + 32 * u;
-                int myrow = rcur;
-                // the rows after rcur that start inside this group (rows are
-                // sorted by their first component; lane = row)
-                uint32_t starts = __ballot_sync(FULL, lane > rcur && lane < rows && f <= base + 31);
-                while (starts) {
-                    const int nr = __ffs(starts) - 1;
-                    starts &= starts - 1;
-                    if (base + lane >= __shfl_sync(FULL, f, nr)) myrow = nr;
-                    rcur = nr;  // starts before the next group's base
-                }
-                rr4[u] = myrow;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                // a group is exactly one word of the non-root bitmap (c = base + lane)
-                const int c = c0 + 32 * u, wi = (gb >> 5) + u;
-                const uint32_t wb = bits[wi];
-                if (c >= ncomp || ((wb >> lane) & 1u)) continue;  // not a root: K4
-                st_keep(complab + c, rb[rr4[u]] + c - (wpre[wi] + __popc(wb & ((1u << lane) - 1u))), keep);
+    // ---- phase 3: label bases of every tile row segment and the labels of
+    // the root border nodes (offset(segment) + rank in segment + 1)
+    const int excl = sm.excl;
+    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
+        const int tile = ty * g.nTx + tx;
+        const int32_t *meta = ws.meta + (int64_t)tile * META;
+        const int nodebase = tile * g.capb;
+        const int nborder = __ldcg(meta + META_NBORDER);
+        const int rf = __ldcg(meta + META_ROWFIRST + lane);
+        const int so = lane < rows ? __ldcg(ws.segoff + (int64_t)(R0 + lane) * g.nTx + tx) : 0;
+        int32_t *tlb = ws.tlb + (int64_t)tile * TH;
+        const int lb = excl + so + __ldcg(tlb + lane) + 1;
+        tlb[lane] = lb;
+        const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+        const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+        for (int j0 = 0; j0 < nborder; j0 += 32) {  // warp-uniform: the shuffles need every lane
+            const int node = nodebase + j0 + lane;
+            const bool valid = j0 + lane < nborder;
+            const bool root = valid && __ldcg(ws.gparent + node) == node;
+            const int gc = valid ? __ldcg(ws.gnodecomp + node) : 0, c = gc & 0xFFFF, row = gc >> 16;
+            const int rfr = __shfl_sync(FULL, rf, row), lbr = __shfl_sync(FULL, lb, row);
+            if (root) {
+                const int nrb =
+                    __ldcg(twpre + (c >> 5)) + __popc(__ldcg(tbits + (c >> 5)) & ((1u << (c & 31)) - 1u));
+                ws.gnodelab[node] = lbr + (c - rfr) - nrb;
             }
         }
     }
-    // labels of the root nodes
-#pragma unroll
-    for (int t = 0; t < KL_NODES; t++) {
-        const int j = lane + 32 * t;
-        if (j < nborder && par[t] == nodebase + j) {
-            const int gc = gcv[t], c = gc & 0xFFFF;
-            ws.gnodelab[nodebase + j] = rb[gc >> 16] + c - nonroots_before(c);
-        }
-    }
-    for (int j = lane + 32 * KL_NODES; j < nborder; j += 32) {
-        const int node = nodebase + j;
-        if (__ldcg(ws.gparent + node) != node) continue;
-        const int gc = __ldcg(ws.gnodecomp + node), c = gc & 0xFFFF;
-        ws.gnodelab[node] = rb[gc >> 16] + c - nonroots_before(c);
-    }
-}
-
-__global__ void __launch_bounds__(KL_WARPS * 32)
-k_label(Geometry g, Workspace ws) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ KLSmem sm;
-    const int lane = lane_id(), w = threadIdx.x >> 5;
-    for (int tile = blockIdx.x * KL_WARPS + w; tile < g.nT; tile += gridDim.x * KL_WARPS) {
-        label_tile(g, ws, sm, tile, w, lane);
-        __syncwarp();  // the warp's shared arrays are reused by its next tile
-    }
+    if (threadIdx.x == 0) ws.rowexcl[ty] = excl;
 }
 
 // ========================================================================= K4
@@ -1243,8 +1160,15 @@ k_fixup(Geometry g, Workspace ws) {
     if (tile >= g.nT) return;
     const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
     const int nodebase = tile * g.capb;
-    int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-    const uint64_t keep = pol_evict_last();  // component labels stay in L2 for K5
+    int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
+    const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+    const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+    const uint64_t keep = pol_evict_last();  // the labels stay in L2 for K5
+    // the non-root's position among the tile's non-root border components
+    // (K3b's bitmap): its slot in nrlab
+    auto slot = [&](int c) -> int {
+        return __ldcg(twpre + (c >> 5)) + __popc(__ldcg(tbits + (c >> 5)) & ((1u << (c & 31)) - 1u));
+    };
     // the parents and components of 4 nodes per lane are loaded at once
     int par[4], gcv[4];
 #pragma unroll
@@ -1256,16 +1180,18 @@ k_fixup(Geometry g, Workspace ws) {
 #pragma unroll
     for (int t = 0; t < 4; t++) {
         if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
+        const int sl = slot(gcv[t] & 0xFFFF);
         const int r = par[t] < 0 ? par[t] : gfind_halve(ws.gparent, par[t]);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(complab + (gcv[t] & 0xFFFF), lab, keep);
+        st_keep(nrlab + sl, lab, keep);
     }
     for (int j = lane + 128; j < nborder; j += 32) {
         const int node = nodebase + j;
         if (__ldcg(ws.gparent + node) == node) continue;
+        const int sl = slot(__ldcg(ws.gnodecomp + node) & 0xFFFF);
         const int r = gfind_halve(ws.gparent, node);
         const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(complab + (__ldcg(ws.gnodecomp + node) & 0xFFFF), lab, keep);
+        st_keep(nrlab + sl, lab, keep);
     }
 }
 
@@ -1295,9 +1221,22 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const int gword = tx * WPR + lane;
     const uint16_t *rc = ws.runcomp + (int64_t)seg * g.maxrun;
     const int32_t off = ws.boff ? __ldcg(ws.boff) : 0;  // labels of earlier row bands
-    // the first 32 run -> component entries are loaded beside the masks (most
-    // rows have fewer runs), so the label gather is the only dependent load
+    // the first 32 run entries are loaded beside the masks (most rows have
+    // fewer runs), and so are the tile's tables, one entry per lane: row
+    // offsets and label bases (lane = tile row), the non-root bitmap and its
+    // prefix (lane = word), the first 64 non-root labels (lane = slot).  All
+    // independent: the labels below are computed with shuffles, no
+    // dependent gather.
     const uint32_t rc0 = lane < g.maxrun ? (uint32_t)__ldcs(rc + lane) : 0u;
+    const int rfv = __ldcg(ws.meta + (int64_t)tile * META + META_ROWFIRST + lane);
+    const int lbv = __ldcg(ws.tlb + (int64_t)tile * TH + lane);
+    const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+    const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+    const int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
+    const uint32_t bwv = lane < g.capw ? __ldcg(tbits + lane) : 0u;
+    const int wpv = lane < g.capw ? __ldcg(twpre + lane) : 0;
+    const int nlv = lane < g.capc ? __ldcg(nrlab + lane) : 0;
+    const int nlv2 = lane + 32 < g.capc ? __ldcg(nrlab + 32 + lane) : 0;
     uint32_t x;                                          // foreground
     const uint32_t f = run_mask(g, ws.bm, row, gword, &x);  // runs
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
@@ -1306,10 +1245,34 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     int32_t *rowlab = s_lab[wi] + 1;
     {
-        const int32_t *complab = ws.complab + (int64_t)tile * g.capc;
-        if (lane < (int)nr) rowlab[lane] = complab[rc0] + off;
+        // label of run entry v = (root row, rank): component c = rowfirst[row]
+        // + rank; a non-root border component takes its slot's label (K4),
+        // any other component tlb[row] + rank - (non-roots before c) (K3b).
+        // Every lane runs the shuffles (entries past the row are harmless).
+        auto run_label = [&](uint32_t v) -> int {
+            const int row = (int)(v >> 9) & 31, rank = (int)(v & 0x1FFu);
+            const int c = __shfl_sync(FULL, rfv, row) + rank, wd = c >> 5;
+            uint32_t w = __shfl_sync(FULL, bwv, wd & 31);
+            int pre = __shfl_sync(FULL, wpv, wd & 31);
+            if (wd >= 32) {  // more than 1024 components in the tile
+                w = __ldcg(tbits + wd);
+                pre = __ldcg(twpre + wd);
+            }
+            const int nb = pre + __popc(w & ((1u << (c & 31)) - 1u));
+            const int lb = __shfl_sync(FULL, lbv, row);
+            const int nla = __shfl_sync(FULL, nlv, nb & 31), nlb = __shfl_sync(FULL, nlv2, nb & 31);
+            const int nl = nb < 32 ? nla : nlb;
+            if (!((w >> (c & 31)) & 1u)) return lb + rank - nb + off;
+            return (nb < 64 ? nl : __ldcg(nrlab + nb)) + off;
+        };
+        const int l0 = run_label(rc0);
+        if (lane < (int)nr) rowlab[lane] = l0;
 #pragma unroll 1
-        for (int k = 32 + lane; k < (int)nr; k += 32) rowlab[k] = complab[__ldcs(rc + k)] + off;
+        for (int k0 = 32; k0 < (int)nr; k0 += 32) {  // warp-uniform: the shuffles need every lane
+            const int k = k0 + lane;
+            const int l = run_label(k < (int)nr ? (uint32_t)__ldcs(rc + k) : 0u);
+            if (k < (int)nr) rowlab[k] = l;
+        }
     }
     s_word[wi][lane] = make_uint4(x, hx, base, 0u);
     __syncwarp();
@@ -1387,9 +1350,11 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
     const uint32_t base = warp_excl_scan(__popc(hx), nr);
     const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * g.maxrun;
     const int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
+    const int32_t *rowfirst = ws.meta + (int64_t)tile * META + META_ROWFIRST;
     // root node and key once per run ...
     for (int k = lane; k < (int)nr; k += 32) {
-        const int node = gfind_ro(ws.gparent, compnode[rc[k]]);
+        const uint32_t v = rc[k];  // (root row << 9) | rank
+        const int node = gfind_ro(ws.gparent, compnode[rowfirst[v >> 9] + (int)(v & 0x1FFu)]);
         s_node[wi][k] = node;
         s_key[wi][k] = ws.gkey[node];
     }
@@ -1498,7 +1463,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 6 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3-K5, K2 if any edge
+    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3-K5, K2 if any edge
 }
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
@@ -1592,9 +1557,6 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
                             cudaStream_t stream, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[K_NUMBER], stream);
     cudaError_t e = launch_pdl(k_number, g.nTy, KN_WARPS * 32, 0, stream, g, ws, n_components);
-    if (e != cudaSuccess) return e;
-    if (ev) cudaEventRecord(ev[K_LABEL], stream);
-    e = launch_pdl(k_label, (g.nT + KL_WARPS * KL_TPW - 1) / (KL_WARPS * KL_TPW), KL_WARPS * 32, 0, stream, g, ws);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

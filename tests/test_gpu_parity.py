@@ -230,7 +230,7 @@ def test_kernel_times_profiling():
     plan.set_profiling(1)
     plan.label(img)
     t = plan.kernel_times()
-    assert set(t) == {"k_tile_local", "k_border", "k_number", "k_label", "k_fixup", "k_write"}
+    assert set(t) == {"k_tile_local", "k_border", "k_number", "k_fixup", "k_write"}
     assert all(v >= 0 for v in t.values())
 
 
