@@ -207,7 +207,7 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
 ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s,
                          cudaEvent_t *ev = nullptr) {
     CK(band_link(b.ws, x.W, self, x.keys, x.spar, b.d_nodes, s));
-    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 1 : nullptr));  // ev[3]
+    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 3 : nullptr));  // ev[3]
     return CCL_OK;
 }
 
@@ -221,7 +221,7 @@ ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int
 // E: labels of merged components (foreign ones from the exported table) + write
 ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s, cudaEvent_t *ev = nullptr) {
     b.ws.xlab = x.exps;
-    CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 2 : nullptr));  // ev[5], ev[6], ev[7]
+    CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 5 : nullptr));  // ev[5], ev[6], ev[7]
     return CCL_OK;
 }
 

@@ -113,6 +113,7 @@ enum {
     STAT_COUNT
 };
 
+// kernels of the single-image pipeline (run_pipeline), for per-kernel events
 enum { K_TILE = 0, K_BORDER, K_NUMBER, K_FIXUP, K_WRITE, K_COUNT };
 extern const char *const kKernelNames[K_COUNT];
 

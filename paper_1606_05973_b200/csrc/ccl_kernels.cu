@@ -420,20 +420,21 @@ __device__ __forceinline__ uint32_t upper_merge_heads(uint32_t hu, uint32_t u, u
 #endif
 // MR: runs per row held in shared memory (K1_MR in k_tile_local, MAXRUN in
 // k_tile_big).  Run (row r, ordinal o) has index k = r*MR + o.
-template <bool THR, bool BATCH, bool BANDS, int MR>
+template <bool THR, bool BATCH, bool BANDS, int MR, int SR = S>
 __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const Geometry &g, const Workspace &ws,
-                                        const int tile, int pfd, int stop) {
+                                        const int tile, const int tx, const int ty, int pfd, int pfx, int pfy,
+                                        int stop) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1SmemT<MR> &sm = *reinterpret_cast<K1SmemT<MR> *>(smem_raw);
     auto kidx = [](int r, int o) { return r * MR + o; };
+    constexpr int NWK = TH / SR;  // warps of the CTA (SR rows each)
 
     const int lane = lane_id(), w = threadIdx.x >> 5;
-    const int tx = tile % g.nTx, ty = tile / g.nTx;
     const int R0 = BATCH ? tile_r0(g, ty) : ty * TH, C0 = tx * TW;
     const int rows = BATCH ? tile_rows(g, ty) : min(TH, g.H - R0);
     const int vcols = min(TW, g.W - C0);
     const int gword = tx * WPR + lane;  // this lane's word index in the image row
-    const int r0 = w * S;
+    const int r0 = w * SR;
     volatile uint16_t *vp = sm.p;
     uint32_t *bbits = &sm.mc[0][0];
 
@@ -442,11 +443,15 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // the device; measured against 3/8, 1/2, 5/8, 1, 1.5 and 2 waves): its
     // loads then hit L2 instead of waiting on HBM.
     {
-        const int pt = tile + pfd;
-        if (pfd > 0 && pt < g.nT) {
-            const int pty = pt / g.nTx;
+        if (pfd > 0 && tile + pfd < g.nT) {
+            // tile + pfd = (ty + pfy, tx + pfx) with a carry (no division)
+            int ptx = tx + pfx, pty = ty + pfy;
+            if (ptx >= g.nTx) {
+                ptx -= g.nTx;
+                pty++;
+            }
             const int prow = (BATCH ? tile_r0(g, pty) : pty * TH) + (threadIdx.x >> 3);
-            const int pcol = (pt % g.nTx) * TW + (threadIdx.x & 7) * 128;
+            const int pcol = ptx * TW + (threadIdx.x & 7) * 128;
             if ((int)(threadIdx.x >> 3) < TH && (BATCH ? (int)(threadIdx.x >> 3) < tile_rows(g, pty) : prow < g.H) &&
                 pcol < g.W) {
                 const uint8_t *a = img + (int64_t)prow * g.W + pcol;
@@ -469,14 +474,14 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     pdl_wait();
     // ---- P0: the pixels of the tile, read once with 16-byte streaming loads:
     // fg = byte != 0 (reading A10) -- or byte > thr when a
-    // threshold is set -- one bit per pixel.  The warp's S rows are all in
+    // threshold is set -- one bit per pixel.  The warp's SR rows are all in
     // flight before the first is used.
-    uint32_t xs[S];
-    if (g.aligned && C0 + TW <= g.W && rows == TH) {  // interior tile: all 2*S loads in flight
+    uint32_t xs[SR];
+    if (g.aligned && C0 + TW <= g.W && rows == TH) {  // interior tile: all 2*SR loads in flight
         const uint8_t *src = img + (int64_t)(R0 + r0) * g.W + C0 + 32 * lane;
-        uint4 v[2 * S];
+        uint4 v[2 * SR];
 #pragma unroll
-        for (int i = 0; i < S; i++) {
+        for (int i = 0; i < SR; i++) {
             v[2 * i] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W));
             v[2 * i + 1] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W + 16));
         }
@@ -484,22 +489,22 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             // warp-uniform fast path when every byte the warp loaded is 0 or 1
             uint32_t o = 0;
 #pragma unroll
-            for (int j = 0; j < 2 * S; j++) o |= v[j].x | v[j].y | v[j].z | v[j].w;
+            for (int j = 0; j < 2 * SR; j++) o |= v[j].x | v[j].y | v[j].z | v[j].w;
             if (!__any_sync(FULL, (o & 0xFEFEFEFEu) != 0u)) {
 #pragma unroll
-                for (int i = 0; i < S; i++) xs[i] = pack16_01(v[2 * i]) | (pack16_01(v[2 * i + 1]) << 16);
+                for (int i = 0; i < SR; i++) xs[i] = pack16_01(v[2 * i]) | (pack16_01(v[2 * i + 1]) << 16);
             } else {
 #pragma unroll
-                for (int i = 0; i < S; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
+                for (int i = 0; i < SR; i++) xs[i] = pack16(v[2 * i]) | (pack16(v[2 * i + 1]) << 16);
             }
         } else {
             const uint32_t t4 = (uint32_t)g.thr * 0x01010101u;
 #pragma unroll
-            for (int i = 0; i < S; i++) xs[i] = pack16_gt(v[2 * i], t4) | (pack16_gt(v[2 * i + 1], t4) << 16);
+            for (int i = 0; i < SR; i++) xs[i] = pack16_gt(v[2 * i], t4) | (pack16_gt(v[2 * i + 1], t4) << 16);
         }
     } else {
 #pragma unroll
-        for (int i = 0; i < S; i++)
+        for (int i = 0; i < SR; i++)
             xs[i] = (r0 + i < rows && gword < g.WW) ? load_word<THR>(img, g, R0 + r0 + i, 32 * gword) : 0u;
     }
     // bm (1/8 B per pixel) is read again by K2 and K5 while ~5 B/px of image
@@ -508,18 +513,18 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     uint64_t pol_last;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
     if (MR < MAXRUN && tile == 0) {  // reset the numbering scan's lookback state (K3)
-        for (int i = threadIdx.x; i < g.nTy; i += NW * 32) ws.scanstate[i] = 0ull;
+        for (int i = threadIdx.x; i < g.nTy; i += NWK * 32) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
     }
 #pragma unroll
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         sm.mc[r0 + i][lane] = xs[i];  // raw masks (mc is free until P2a)
         if (r0 + i < rows && gword < g.WW) {
             asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(ws.bm + (int64_t)(R0 + r0 + i) * g.WW + gword),
                          "r"(xs[i]), "l"(pol_last) : "memory");
         }
     }
-    if (lane < S) sm.bcnt[r0 + lane] = 0;
+    if (lane < SR) sm.bcnt[r0 + lane] = 0;
     if (threadIdx.x == 0) sm.nmerge = 0;
     __syncthreads();
     K1_STOP(stop < 0);
@@ -532,7 +537,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // label.
     bool over = false;  // a row of this warp has more runs than the p array holds
 #pragma unroll
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         const int rl = r0 + i;
         const uint32_t x0 = xs[i];
         const uint32_t xlr = __shfl_up_sync(FULL, x0, 1), xrr = __shfl_down_sync(FULL, x0, 1);
@@ -575,7 +580,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // parent (already final within the strip); a strip's first row copies the
     // upper run's index (a run of the strip above).
 #pragma unroll 1
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         const int rl = r0 + i;
         if (rl >= rows || rl == 0) {
             sm.mc[rl][lane] = 0u;
@@ -649,16 +654,16 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     }
     // All 256 threads work through the list at once (union_smem is safe
     // under concurrency, see above).
-    for (int i = threadIdx.x; i < min(nmerge, MLC); i += NW * 32) {
+    for (int i = threadIdx.x; i < min(nmerge, MLC); i += NWK * 32) {
         const uint32_t e = sm.mlist[i], a = e & 0xFFFFu, c = e >> 16;
         if (vp[a] != vp[c]) union_smem(sm.p, a, c);
     }
     if (nmerge <= MLC) {  // nothing left per lane: clear the rows for bbits
 #pragma unroll
-        for (int i = 0; i < S; i++) sm.mc[r0 + i][lane] = 0u;
+        for (int i = 0; i < SR; i++) sm.mc[r0 + i][lane] = 0u;
     } else
 #pragma unroll 1
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         const int rl = r0 + i;
         uint32_t m = (rl < rows) ? sm.mc[rl][lane] : 0u;
         sm.mc[rl][lane] = 0u;  // becomes this row's part of bbits
@@ -688,7 +693,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // count (row of run r = r / MAXRUN).
     const int lc = vcols - 1;
 #pragma unroll 1
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
         const bool edge_row = rl == 0 || rl == rows - 1;
         const bool lfirst = sm.bm[rl][0] & 1u, llast = (sm.bm[rl][lc >> 5] >> (lc & 31)) & 1u;
@@ -740,7 +745,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
 #pragma unroll 1
-    for (int i = 0; i < S; i++) {
+    for (int i = 0; i < SR; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
         int bi = __shfl_sync(FULL, bfirst, rl);
@@ -788,19 +793,19 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             return nodebase + sm.hbase[rr][ro >> 5] + __popc(bbits[rr * WPR + (ro >> 5)] & ((1u << (ro & 31)) - 1u));
         };
         const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
-        for (int o = threadIdx.x; o < ntop; o += NW * 32)
+        for (int o = threadIdx.x; o < ntop; o += NWK * 32)
             ws.topnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(0, o));
-        for (int o = threadIdx.x; o < nbot; o += NW * 32)
+        for (int o = threadIdx.x; o < nbot; o += NWK * 32)
             ws.botnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(rows - 1, o));
-        for (int r = threadIdx.x; r < rows; r += NW * 32) {
+        for (int r = threadIdx.x; r < rows; r += NWK * 32) {
             const int64_t off = (int64_t)tx * g.H + R0 + r;
             ws.leftnode[off] = (sm.bm[r][0] & 1u) ? node_of(kidx(r, 0)) : -1;
             ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? node_of(kidx(r, sm.nrun[r] - 1)) : -1;
         }
     }
     // the first and last row's run masks for K2's horizontal edges
-    if (w == NW - 1) ws.edgerow[(int64_t)tile * 2 * WPR + lane] = sm.bm[0][lane];
-    if (w == NW - 2) ws.edgerow[((int64_t)tile * 2 + 1) * WPR + lane] = sm.bm[rows - 1][lane];
+    if (w == NWK - 1) ws.edgerow[(int64_t)tile * 2 * WPR + lane] = sm.bm[0][lane];
+    if (w == NWK - 2) ws.edgerow[((int64_t)tile * 2 + 1) * WPR + lane] = sm.bm[rows - 1][lane];
     int32_t *meta = ws.meta + (int64_t)tile * META;
     if (w == 0) {  // first component of every tile row (components are in key order)
         meta[META_ROWFIRST + lane] = rowfirst;
@@ -815,9 +820,32 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
 
 template <bool THR, bool BATCH, bool BANDS = false>
 __global__ void __launch_bounds__(NW * 32, 6)
-k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int stop) {
+k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int pfx, int pfy, int stop) {
     pdl_trigger();
-    k1_tile<THR, BATCH, BANDS, K1_MR>(img, g, ws, blockIdx.x, pfd, stop);
+    // a 2-D grid (tile columns x tile rows; CTAs still start in raster
+    // order) spares the divisions, unless nTy exceeds the grid's y limit
+    int tile, tx, ty;
+    if (gridDim.y > 1 || g.nTy == 1) {
+        tx = blockIdx.x;
+        ty = blockIdx.y;
+        tile = ty * g.nTx + tx;
+    } else {
+        tile = blockIdx.x;
+        tx = tile % g.nTx;
+        ty = tile / g.nTx;
+    }
+    k1_tile<THR, BATCH, BANDS, K1_MR>(img, g, ws, tile, tx, ty, pfd, pfx, pfy, stop);
+}
+
+// Images of few tiles (fewer than the SMs can hold twice over): one warp per
+// tile row, 32 warps per CTA, so a tile's rows are worked on in parallel --
+// the single-image latency of the <= 1 MB regime.
+template <bool THR, bool BATCH, bool BANDS = false>
+__global__ void __launch_bounds__(TH * 32, 1)
+k_tile_local_wide(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) {
+    pdl_trigger();
+    const int tile = blockIdx.x;
+    k1_tile<THR, BATCH, BANDS, K1_MR, 1>(img, g, ws, tile, tile % g.nTx, tile / g.nTx, 0, 0, 0, stop);
 }
 
 // The tiles k_tile_local handed over (a row with more than K1_MR runs); the
@@ -829,7 +857,8 @@ k_tile_big(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) 
     pdl_wait();
     const int n = __ldcg(ws.k1over_n);
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        k1_tile<THR, BATCH, BANDS, MAXRUN>(img, g, ws, __ldcg(ws.k1over + i), 0, stop);
+        const int tile = __ldcg(ws.k1over + i);
+        k1_tile<THR, BATCH, BANDS, MAXRUN>(img, g, ws, tile, tile % g.nTx, tile / g.nTx, 0, 0, 0, stop);
         __syncthreads();  // shared memory is reused by the next tile
     }
 }
@@ -841,7 +870,7 @@ k_tile_big(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) 
 // corner pixels): one thread per (tile column boundary, row).
 constexpr int K2_WARPS = 4;  // measured vs 2 and 8 warps per CTA
 __global__ void __launch_bounds__(K2_WARPS * 32)
-k_border(Geometry g, Workspace ws, int nh_warps) {
+k_border(Geometry g, Workspace ws, int nh_warps, int hsplit) {
     pdl_trigger();
     pdl_wait();
     __shared__ uint32_t shd[K2_WARPS][2][WPR], sbs[K2_WARPS][2][WPR];
@@ -850,7 +879,10 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * K2_WARPS + wib;
     if (gw < nh_warps) {
-        const int tx = gw % g.nTx, ty = 1 + gw / g.nTx;
+        // hsplit warps per horizontal edge (images of few tiles: more lanes
+        // for the edge's unions); each lists them all and works on its share
+        const int he = gw / hsplit, hs = gw - he * hsplit;
+        const int tx = he % g.nTx, ty = 1 + he / g.nTx;
         if (ty % g.tpi == 0) return;  // first tile row of an image of a batch: no edge
         // the run masks of the two rows, as K1 left them
         const uint32_t u = __ldcg(ws.edgerow + ((int64_t)((ty - 1) * g.nTx + tx) * 2 + 1) * WPR + lane);
@@ -899,7 +931,7 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
             }
             __syncwarp();
             const int np = min(PCAP, (int)tot - w0);
-            for (int i = lane; i < np; i += 32) {
+            for (int i = 32 * hs + lane; i < np; i += 32 * hsplit) {
                 const uint32_t e = plist[wib][i];
                 gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
             }
@@ -940,6 +972,69 @@ k_border(Geometry g, Workspace ws, int nh_warps) {
     // diagonal neighbours; skipped when the adjacent row makes the same union
     if (bu >= 0 && !(up_ok && ap == a && bp == bu)) gunion(ws.gparent, ws.gkey, a, bu);
     if (bd >= 0 && !(dn_ok && an == a && bn == bd)) gunion(ws.gparent, ws.gkey, a, bd);
+}
+
+// ========================================================================= K4
+// A border component that is not a global root takes its root's label (a
+// root of this image's forest, or -- row bands -- a root owned by another
+// band, whose global label arrived in xlab; labels stored here are band-local,
+// K5 adds the band offset).  One warp per tile, over its border nodes.
+#ifndef CCL_K4_WARPS
+#define CCL_K4_WARPS 4  // measured vs 2, 8, 16: -0.5 us
+#endif
+constexpr int K4_WARPS = CCL_K4_WARPS;
+// K4's work for one tile (one warp).  (Folded into K3 -- one warp per
+// tile-row CTA works through 2-3 tiles' finds one after another, with flags
+// for the earlier rows' root labels -- it took C4 K3 + K4 from 39 to 56 us.)
+__device__ __forceinline__ void fixup_tile(const Geometry &g, const Workspace &ws, const int tile, const int lane) {
+    const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
+    const int nodebase = tile * g.capb;
+    int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
+    const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+    const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+    const uint64_t keep = pol_evict_last();  // the labels stay in L2 for K5
+    auto root_label = [&](int r) -> int32_t {
+        if (r < 0) return __ldcg(ws.xlab + (-2 - r)) - *ws.boff;  // a root owned by another band
+        return __ldcg(ws.gnodelab + r);
+    };
+    // the non-root's position among the tile's non-root border components
+    // (K3b's bitmap): its slot in nrlab
+    auto slot = [&](int c) -> int {
+        return __ldcg(twpre + (c >> 5)) + __popc(__ldcg(tbits + (c >> 5)) & ((1u << (c & 31)) - 1u));
+    };
+    // the parents and components of 4 nodes per lane are loaded at once
+    int par[4], gcv[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        const int j = lane + 32 * t;
+        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
+        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+        if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
+        const int sl = slot(gcv[t] & 0xFFFF);
+        const int r = par[t] < 0 ? par[t] : gfind_halve(ws.gparent, par[t]);
+        const int32_t lab = root_label(r);
+        st_keep(nrlab + sl, lab, keep);
+    }
+    for (int j = lane + 128; j < nborder; j += 32) {
+        const int node = nodebase + j;
+        if (__ldcg(ws.gparent + node) == node) continue;
+        const int sl = slot(__ldcg(ws.gnodecomp + node) & 0xFFFF);
+        const int r = gfind_halve(ws.gparent, node);
+        const int32_t lab = root_label(r);
+        st_keep(nrlab + sl, lab, keep);
+    }
+}
+
+__global__ void __launch_bounds__(K4_WARPS * 32)
+k_fixup(Geometry g, Workspace ws) {
+    pdl_trigger();
+    pdl_wait();
+    const int tile = blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
+    if (tile >= g.nT) return;
+    fixup_tile(g, ws, tile, lane_id());
 }
 
 // ========================================================================= K3
@@ -1140,59 +1235,6 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     if (threadIdx.x == 0) ws.rowexcl[ty] = excl;
-}
-
-// ========================================================================= K4
-// A border component that is not a global root takes its root's label (a
-// root of this image's forest, or -- row bands -- a root owned by another
-// band, whose global label arrived in xlab; labels stored here are band-local,
-// K5 adds the band offset).  One warp per tile, over its border nodes.
-#ifndef CCL_K4_WARPS
-#define CCL_K4_WARPS 4  // measured vs 2, 8, 16: -0.5 us
-#endif
-constexpr int K4_WARPS = CCL_K4_WARPS;
-__global__ void __launch_bounds__(K4_WARPS * 32)
-k_fixup(Geometry g, Workspace ws) {
-    pdl_trigger();
-    pdl_wait();
-    const int lane = lane_id();
-    const int tile = blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
-    if (tile >= g.nT) return;
-    const int nborder = __ldcg(ws.meta + (int64_t)tile * META + META_NBORDER);
-    const int nodebase = tile * g.capb;
-    int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
-    const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
-    const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
-    const uint64_t keep = pol_evict_last();  // the labels stay in L2 for K5
-    // the non-root's position among the tile's non-root border components
-    // (K3b's bitmap): its slot in nrlab
-    auto slot = [&](int c) -> int {
-        return __ldcg(twpre + (c >> 5)) + __popc(__ldcg(tbits + (c >> 5)) & ((1u << (c & 31)) - 1u));
-    };
-    // the parents and components of 4 nodes per lane are loaded at once
-    int par[4], gcv[4];
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-        const int j = lane + 32 * t;
-        par[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : nodebase + j;
-        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
-    }
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-        if (par[t] == nodebase + lane + 32 * t) continue;  // a root (or past nborder)
-        const int sl = slot(gcv[t] & 0xFFFF);
-        const int r = par[t] < 0 ? par[t] : gfind_halve(ws.gparent, par[t]);
-        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(nrlab + sl, lab, keep);
-    }
-    for (int j = lane + 128; j < nborder; j += 32) {
-        const int node = nodebase + j;
-        if (__ldcg(ws.gparent + node) == node) continue;
-        const int sl = slot(__ldcg(ws.gnodecomp + node) & 0xFFFF);
-        const int r = gfind_halve(ws.gparent, node);
-        const int32_t lab = r >= 0 ? __ldcg(ws.gnodelab + r) : __ldcg(ws.xlab + (-2 - r)) - *ws.boff;
-        st_keep(nrlab + sl, lab, keep);
-    }
 }
 
 // ========================================================================= K5
@@ -1463,7 +1505,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3-K5, K2 if any edge
+    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3, K4, K5, K2 if any edge
 }
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
@@ -1483,6 +1525,23 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned bl
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// The same with a 2-D grid.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t stream,
+                               Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static int g_k1big_resident = 0;
 static cudaError_t set_attrs() {
@@ -1490,6 +1549,12 @@ static cudaError_t set_attrs() {
     cudaError_t e = cudaSuccess;
     for (auto k : {k_tile_local<false, false>, k_tile_local<true, false>, k_tile_local<false, true>,
                    k_tile_local<true, true>, k_tile_local<false, false, true>, k_tile_local<true, false, true>})
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
+            return e;
+    for (auto k : {k_tile_local_wide<false, false>, k_tile_local_wide<true, false>, k_tile_local_wide<false, true>,
+                   k_tile_local_wide<true, true>, k_tile_local_wide<false, false, true>,
+                   k_tile_local_wide<true, false, true>})
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
             return e;
@@ -1532,10 +1597,23 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     };
     mark(K_TILE);
     const bool batch = g.tpi != g.nTy, bands = ws.boff != nullptr;  // (a band workspace has its offset)
-    auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
-                    : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
-    e = launch_pdl(k1, g.nT, NW * 32, sizeof(K1SmemT<K1_MR>), stream, img, g, ws,
-                   g_k1_exper ? 0 : g_k1_resident / 4, g_k1_stop);
+    // few tiles: the 32-warp K1 (one warp per tile row) shortens the tile's
+    // latency; many tiles: the 8-warp K1 (6 CTAs per SM) keeps the SMs busy
+    const bool wide = g.nT * 4 <= g_k1_resident;
+    if (wide) {
+        auto k1 = g.thr ? (batch ? k_tile_local_wide<true, true> : bands ? k_tile_local_wide<true, false, true>
+                                                                        : k_tile_local_wide<true, false>)
+                        : (batch ? k_tile_local_wide<false, true> : bands ? k_tile_local_wide<false, false, true>
+                                                                         : k_tile_local_wide<false, false>);
+        e = launch_pdl(k1, g.nT, TH * 32, sizeof(K1SmemT<K1_MR>), stream, img, g, ws, g_k1_stop);
+    } else {
+        auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
+                        : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
+        const int pfd = g_k1_exper ? 0 : g_k1_resident / 4;
+        const bool twod = g.nTy <= 65535;
+        e = launch_pdl2(k1, twod ? dim3(g.nTx, g.nTy) : dim3(g.nT), NW * 32, sizeof(K1SmemT<K1_MR>), stream, img, g,
+                        ws, pfd, pfd % g.nTx, pfd / g.nTx, g_k1_stop);
+    }
     if (e != cudaSuccess) return e;
     auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
                      : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
@@ -1546,38 +1624,47 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     if (g_k1_stop < 99) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    const int64_t warps = nh + (nv + 31) / 32;
+    // few horizontal edges (small images): 4 warps share each edge's unions
+    const int hsplit = nh * 4 * 4 <= g_k1_resident * 8 ? 4 : 1;
+    const int64_t warps = (int64_t)nh * hsplit + (nv + 31) / 32;
     if (warps > 0)
-        e = launch_pdl(k_border, (unsigned)((warps + K2_WARPS - 1) / K2_WARPS), K2_WARPS * 32, 0, stream, g, ws, nh);
+        e = launch_pdl(k_border, (unsigned)((warps + K2_WARPS - 1) / K2_WARPS), K2_WARPS * 32, 0, stream, g, ws,
+                       nh * hsplit, hsplit);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
+// K3 (N and the root labels; on the row-band path K4 runs after the
+// cross-band export).  Event (optional): ev[0] before K3.
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev) {
-    if (ev) cudaEventRecord(ev[K_NUMBER], stream);
+    if (ev) cudaEventRecord(ev[0], stream);
     cudaError_t e = launch_pdl(k_number, g.nTy, KN_WARPS * 32, 0, stream, g, ws, n_components);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-cudaError_t run_stage_final(const Geometry &g0, const Workspace &ws, int32_t *labels,
-                            cudaStream_t stream, cudaEvent_t *ev) {
+static cudaError_t launch_write(const Geometry &g0, const Workspace &ws, int32_t *labels, cudaStream_t stream) {
     const Geometry g = with_ptr_alignment(g0, labels);
-    auto mark = [&](int i) {
-        if (ev) cudaEventRecord(ev[i], stream);
-    };
-    mark(K_FIXUP);
+    return launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream,
+                      g, ws, labels);
+}
+
+// K4 + K5.  Events (optional): ev[0] before K4, ev[1] before K5, ev[2] after.
+cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
+                            cudaStream_t stream, cudaEvent_t *ev) {
+    if (ev) cudaEventRecord(ev[0], stream);
     cudaError_t e = launch_pdl(k_fixup, (g.nT + K4_WARPS - 1) / K4_WARPS, K4_WARPS * 32, 0, stream, g, ws);
     if (e != cudaSuccess) return e;
-    mark(K_WRITE);
-    e = launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0,
-                   stream, g, ws, labels);
+    if (ev) cudaEventRecord(ev[1], stream);
+    e = launch_write(g, ws, labels, stream);
     if (e != cudaSuccess) return e;
-    mark(K_COUNT);
+    if (ev) cudaEventRecord(ev[2], stream);
     return cudaGetLastError();
 }
 
+// Single image / batch: K1 (+ its hand-over pass), K2, K3, K4, K5.  Events
+// (optional, K_COUNT + 1): ev[i] before kernel i, ev[K_COUNT] after.
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev) {
@@ -1586,8 +1673,8 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
         for (int i = K_NUMBER; ev && i <= K_COUNT; i++) cudaEventRecord(ev[i], stream);
         return e;
     }
-    if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev);
-    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev);
+    if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev ? ev + K_NUMBER : nullptr);
+    if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev ? ev + K_FIXUP : nullptr);
     return e;
 }
 
