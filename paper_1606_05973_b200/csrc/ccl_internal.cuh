@@ -22,7 +22,7 @@ constexpr int META = 40;               // ints of per-tile metadata
 constexpr int META_NCOMP = 0, META_NBORDER = 1, META_ROWS = 2;
 constexpr int META_ROWFIRST = 4;       // [TH+1] first component index of each tile row
 
-constexpr int KN_WARPS = 8;            // k_number: warps per tile-row CTA
+constexpr int KN_WARPS = 8;            // k_number: warps per tile-row CTA (fewer for narrow images)
 constexpr int KN_ITEMS = 4;            // k_number: segments per thread per scan chunk
 
 struct Geometry {

@@ -1057,19 +1057,23 @@ k_fixup(Geometry g, Workspace ws) {
 //                  nonroots_before(c);
 //   gnodelab       the labels of the tile's root border nodes (K4 reads them
 //                  for the components merged into them).
+template <int NWN>
 struct KNSmem {
-    int32_t nrrow[KN_WARPS][TH];           // non-root border components per row
-    uint32_t bits[KN_WARPS][CAPC / 32];    // the warp's tile's non-root bitmap
-    int32_t wsum[KN_WARPS];
+    int32_t nrrow[NWN][TH];           // non-root border components per row
+    uint32_t bits[NWN][CAPC / 32];    // the warp's tile's non-root bitmap
+    int32_t wsum[NWN];
     int32_t part, excl;
 };
 
-__global__ void __launch_bounds__(KN_WARPS * 32, 6)
+// NWN warps per tile-row CTA (8; fewer for images of 1-4 tile columns, so
+// the idle warps do not hold SM slots: C2 batches of 1024-px-wide images).
+template <int NWN>
+__global__ void __launch_bounds__(NWN * 32, NWN == 8 ? 6 : 16)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
     pdl_trigger();
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
-    __shared__ KNSmem sm;
+    __shared__ KNSmem<NWN> sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
     __syncthreads();
@@ -1078,7 +1082,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     const bool first = ty % g.tpi == 0;  // first tile row of its image: numbering starts at 1
     // ---- phase 1: non-root border components of every tile (bitmap, prefix,
     // counts per row) and the root counts of the segments (R0 + r, tx)
-    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
+    for (int tx = w; tx < g.nTx; tx += NWN) {
         const int tile = ty * g.nTx + tx;
         const int32_t *meta = ws.meta + (int64_t)tile * META;
         const int nodebase = tile * g.capb;
@@ -1144,7 +1148,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     const int64_t sbase = (int64_t)R0 * g.nTx;
     const int nS = rows * g.nTx;
     int carry = 0;
-    for (int c0 = 0; c0 < nS; c0 += KN_WARPS * 32 * KN_ITEMS) {
+    for (int c0 = 0; c0 < nS; c0 += NWN * 32 * KN_ITEMS) {
         const int i0 = c0 + threadIdx.x * KN_ITEMS;
         int v[KN_ITEMS], sum = 0;
 #pragma unroll
@@ -1158,7 +1162,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         __syncthreads();
         int off = 0, all = 0;
 #pragma unroll
-        for (int i = 0; i < KN_WARPS; i++) {
+        for (int i = 0; i < NWN; i++) {
             off += i < w ? sm.wsum[i] : 0;
             all += sm.wsum[i];
         }
@@ -1209,7 +1213,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     // ---- phase 3: label bases of every tile row segment and the labels of
     // the root border nodes (offset(segment) + rank in segment + 1)
     const int excl = sm.excl;
-    for (int tx = w; tx < g.nTx; tx += KN_WARPS) {
+    for (int tx = w; tx < g.nTx; tx += NWN) {
         const int tile = ty * g.nTx + tx;
         const int32_t *meta = ws.meta + (int64_t)tile * META;
         const int nodebase = tile * g.capb;
@@ -1302,10 +1306,13 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
             }
             const int nb = pre + __popc(w & ((1u << (c & 31)) - 1u));
             const int lb = __shfl_sync(FULL, lbv, row);
-            const int nla = __shfl_sync(FULL, nlv, nb & 31), nlb = __shfl_sync(FULL, nlv2, nb & 31);
-            const int nl = nb < 32 ? nla : nlb;
-            if (!((w >> (c & 31)) & 1u)) return lb + rank - nb + off;
-            return (nb < 64 ? nl : __ldcg(nrlab + nb)) + off;
+            const bool nonroot = (w >> (c & 31)) & 1u;
+            int lab = lb + rank - nb;
+            if (__any_sync(FULL, nonroot)) {  // warp-uniform: most chunks have no merged border component
+                const int nla = __shfl_sync(FULL, nlv, nb & 31), nlb = __shfl_sync(FULL, nlv2, nb & 31);
+                if (nonroot) lab = nb < 32 ? nla : (nb < 64 ? nlb : __ldcg(nrlab + nb));
+            }
+            return lab + off;
         };
         const int l0 = run_label(rc0);
         if (lane < (int)nr) rowlab[lane] = l0;
@@ -1542,7 +1549,8 @@ static cudaError_t launch_pdl2(void (*kern)(KArgs...), dim3 grid, unsigned block
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-static int g_k1_resident = 0;  // K1 CTAs resident on the device at once (L2 prefetch distance)
+static int g_k1_resident = 0;
+static int g_sms = 148;  // K1 CTAs resident on the device at once (L2 prefetch distance)
 static int g_k1big_resident = 0;
 static cudaError_t set_attrs() {
     if (g_attr_done) return cudaSuccess;
@@ -1570,6 +1578,7 @@ static cudaError_t set_attrs() {
                                                            sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
         return e;
     g_k1_resident = sms * per;
+    g_sms = sms;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_big<false, false>, NW * 32,
                                                            sizeof(K1Smem))) != cudaSuccess)
         return e;
@@ -1624,8 +1633,10 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     if (g_k1_stop < 99) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    // few horizontal edges (small images): 4 warps share each edge's unions
-    const int hsplit = nh * 4 * 4 <= g_k1_resident * 8 ? 4 : 1;
+    // few horizontal edges (small images, batches of them): 2 or 4 warps
+    // share each edge's unions while the warps still fit on the device at once
+    const int64_t vwarps = (nv + 31) / 32, slots = (int64_t)g_sms * 64;
+    const int hsplit = ((int64_t)nh * 4 + vwarps <= slots) ? 4 : ((int64_t)nh * 2 + vwarps <= slots) ? 2 : 1;
     const int64_t warps = (int64_t)nh * hsplit + (nv + 31) / 32;
     if (warps > 0)
         e = launch_pdl(k_border, (unsigned)((warps + K2_WARPS - 1) / K2_WARPS), K2_WARPS * 32, 0, stream, g, ws,
@@ -1639,7 +1650,10 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], stream);
-    cudaError_t e = launch_pdl(k_number, g.nTy, KN_WARPS * 32, 0, stream, g, ws, n_components);
+    const int nw = g.nTx >= 8 ? 8 : g.nTx >= 4 ? 4 : g.nTx >= 2 ? 2 : 1;
+    void (*k3)(Geometry, Workspace, int32_t *) =
+        nw == 8 ? k_number<8> : nw == 4 ? k_number<4> : nw == 2 ? k_number<2> : k_number<1>;
+    cudaError_t e = launch_pdl(k3, g.nTy, nw * 32, 0, stream, g, ws, n_components);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
