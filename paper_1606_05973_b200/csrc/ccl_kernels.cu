@@ -749,6 +749,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         const int rl = r0 + i, n = sm.nrun[rl];
         uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
         int bi = __shfl_sync(FULL, bfirst, rl);
+        const int rf = __shfl_sync(FULL, rowfirst, rl);
         const bool hasb = sm.bcnt[rl] != 0;
         const uint32_t *brow = bbits + rl * WPR;
 #pragma unroll 1
@@ -757,7 +758,6 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             const uint32_t pk = o < n ? sm.p[k] : 0u;
             const int r = (pk & 0x8000u) ? k : (int)pk;
             const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
-            const int c = __shfl_sync(FULL, rowfirst, r / MR) + (int)(pr & 0x1FFu);
             if (o < n) {
                 // runcomp = (root row << 9) | rank of the root in its row; the
                 // component is rowfirst[row] + rank (K5 needs the row)
@@ -769,7 +769,8 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
                 if (lane == 0) sm.hbase[rl][o0 >> 5] = (uint16_t)bi;
                 const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
                 const uint32_t bbal = __ballot_sync(FULL, broot);
-                if (broot) {
+                if (broot) {  // a root of this row: component rowfirst[row] + rank
+                    const int c = rf + (int)(pk & 0x1FFu);
                     const int node = nodebase + bi + __popc(bbal & ((1u << lane) - 1u));
                     if (BANDS) compnode[c] = node;  // only the row-band path reads it
                     ws.gparent[node] = node;

@@ -31,6 +31,11 @@ for N in [1, 2, 4, 8]:
     for _ in range(20): plan.label(band, out, n)
     torch.cuda.synchronize()
     kt = plan.kernel_times(); plan.set_profiling(0)
+    sp.set_profiling(20)
+    for _ in range(20): sp.label(band, out, n)
+    torch.cuda.synchronize()
+    st = sp.kernel_times(); sp.set_profiling(0)
     print(f"N={N}: band {bh}x{W}: plan {tp*1e3:.1f} us, band path (1 rank) {ts*1e3:.1f} us, "
           f"projected whole-image {H*W/(ts*1e-3)/1e9:.0f} Gpx/s before the exchange; kernels "
-          + " ".join(f"{k} {v*1e3:.1f}" for k, v in kt.items()), flush=True)
+          + " ".join(f"{k} {v*1e3:.1f}" for k, v in kt.items())
+          + "; band-path stages " + " ".join(f"{k} {v*1e3:.1f}" for k, v in st.items()), flush=True)
