@@ -128,7 +128,7 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
 // this image/band -> *n_components); final = labels of merged components +
 // label write.
 cudaError_t run_stage_local(const Geometry &g, const Workspace &ws, const uint8_t *img,
-                            cudaStream_t stream, cudaEvent_t *ev);
+                            cudaStream_t stream, cudaEvent_t *ev, bool with_border = true);
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev);
 cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,

@@ -1242,6 +1242,291 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     if (threadIdx.x == 0) ws.rowexcl[ty] = excl;
 }
 
+// ============================================================ small images
+// K2 + K3 + K4 in ONE CTA for images of one tile column and at most 32 tile
+// rows (W <= 1024, H <= 1024: the paper's <= 1 MB regime, PAPER.md:1172-
+// 1177).  Every border node's parent lives in shared memory, so the tile-edge
+// unions, the flatten, the numbering (one block scan over the image rows; no
+// lookback) and the non-root labels cost shared-memory latency instead of a
+// chain of five global-memory kernels.  With one tile column the node index
+// order IS the raster key order (tiles stacked vertically, nodes of a tile in
+// raster order), so the union links by index.  Outputs are those of K2-K4:
+// tbits / twpre / tlb / gnodelab / nrlab and N.
+constexpr int SMALL_MAX_TILES = 32;  // one warp per tile
+constexpr int SMALL_MAX_ROWS = 1024; // one thread per image row in the scan
+constexpr int SMALL_THREADS = 1024;
+__device__ __forceinline__ int sfind(volatile int32_t *par, int x) {
+    while (true) {
+        const int px = par[x];
+        if (px == x) return x;
+        const int ppx = par[px];
+        if (ppx == px) return px;
+        par[x] = ppx;  // path halving: an ancestor
+        x = ppx;
+    }
+}
+__device__ __forceinline__ void sunion(int32_t *par, int a, int b) {
+    volatile int32_t *vp = par;
+    a = sfind(vp, a);
+    b = sfind(vp, b);
+    while (a != b) {
+        if (a < b) { const int t = a; a = b; b = t; }
+        const int o = atomicCAS(par + a, a, b);  // link the larger root under the smaller (see union_smem)
+        if (o == a) return;
+        a = sfind(vp, o);
+        b = sfind(vp, b);
+    }
+}
+__global__ void __launch_bounds__(SMALL_THREADS, 1)
+k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ int32_t s_seg[SMALL_MAX_ROWS];       // root count per image row, then its exclusive prefix
+    __shared__ int32_t s_nb[SMALL_MAX_TILES];       // border nodes per tile
+    __shared__ int32_t s_nrp[SMALL_MAX_TILES][TH];  // non-roots in earlier rows of the tile
+    __shared__ int32_t s_wsum[SMALL_THREADS / 32];
+    __shared__ uint32_t s_hx[SMALL_MAX_TILES][2][WPR], s_hb[SMALL_MAX_TILES][2][WPR];
+    __shared__ uint32_t s_pl[SMALL_MAX_TILES][128];  // an edge's unions (upper | lower run ordinal << 16)
+    int32_t *par = reinterpret_cast<int32_t *>(smem_raw);  // nT * capb node parents
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int nT = g.nT, capb = g.capb;
+    if (threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
+    if (threadIdx.x < nT) s_nb[threadIdx.x] = __ldcg(ws.meta + (int64_t)threadIdx.x * META + META_NBORDER);
+    __syncthreads();
+    // the tile's border nodes (only those are ever read), one warp per tile,
+    // four independent loads per lane in flight
+    if (w < nT) {
+        const int nodebase = w * capb, nborder = s_nb[w];
+        for (int j0 = 0; j0 < nborder; j0 += 128) {
+            int v[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int j = j0 + 32 * t + lane;
+                v[t] = j < nborder ? __ldcg(ws.gparent + nodebase + j) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int j = j0 + 32 * t + lane;
+                if (j < nborder) par[nodebase + j] = v[t];
+            }
+        }
+    }
+    __syncthreads();
+    // ---- K2: the horizontal tile edges (one tile column: no vertical ones),
+    // the same two edge families as k_border; unions straight in shared memory
+    if (w >= 1 && w < nT) {
+        const int ty = w;
+        const uint32_t u = __ldcg(ws.edgerow + ((int64_t)(ty - 1) * 2 + 1) * WPR + lane);
+        const uint32_t x = __ldcg(ws.edgerow + (int64_t)ty * 2 * WPR + lane);
+        RowView U = make_row(u), X = make_row(x);
+        s_hx[w][0][lane] = U.hx; s_hb[w][0][lane] = U.base;
+        s_hx[w][1][lane] = X.hx; s_hb[w][1][lane] = X.base;
+        __syncwarp();
+        const int32_t *bot = ws.botnode + (int64_t)(ty - 1) * g.maxrun;
+        const int32_t *top = ws.topnode + (int64_t)ty * g.maxrun;
+        // listed first (consecutive positions per lane by a warp scan), then
+        // in windows of 128: all node loads of a window in flight, then the
+        // shared-memory unions
+        const uint32_t m1 = first_in_run(x & dilate(U), x);
+        uint32_t m2;
+        {
+            const uint32_t t = x & dilate(U);
+            const uint32_t sm_ = smear_up(t, x);
+            const uint32_t cin = carry_in_fwd(((x >> 31) & (sm_ >> 31)) != 0, x == FULL) & x & 1u;
+            m2 = upper_merge_heads(U.hx, u, U.xp, x, X.xp, sm_ | (cin ? (x & ~(x + 1)) : 0u));
+        }
+        uint32_t tot;
+        const int base = (int)warp_excl_scan(__popc(m1) + __popc(m2), tot);
+        uint32_t *pl = s_pl[w];
+        for (int w0 = 0; w0 < (int)tot; w0 += 128) {
+            int idx = base - w0;
+            for (uint32_t m = m1; m && idx < 128; m &= m - 1, idx++) {
+                if (idx < 0) continue;
+                const int b = __ffs(m) - 1;
+                const int q = 32 * lane + b + leftmost3(u, U.xp, U.xn, b), lq = q >> 5;
+                pl[idx] = (uint32_t)run_ord(s_hx[w][0][lq], s_hb[w][0][lq], q & 31) |
+                          ((uint32_t)run_ord(X.hx, X.base, b) << 16);
+            }
+            for (uint32_t m = m2; m && idx < 128; m &= m - 1, idx++) {
+                if (idx < 0) continue;
+                const int b = __ffs(m) - 1;
+                const int q = 32 * lane + b - 1, lq = q >> 5;  // lower pixel h-1
+                pl[idx] = (uint32_t)run_ord(U.hx, U.base, b) |
+                          ((uint32_t)run_ord(s_hx[w][1][lq], s_hb[w][1][lq], q & 31) << 16);
+            }
+            __syncwarp();
+            const int np = min(128, (int)tot - w0);
+            int na[4], nbn[4];
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int i = 32 * t + lane;
+                const uint32_t e = i < np ? pl[i] : 0u;
+                na[t] = i < np ? __ldcg(bot + (e & 0xFFFFu)) : 0;
+                nbn[t] = i < np ? __ldcg(top + (e >> 16)) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; t++)
+                if (32 * t + lane < np) sunion(par, na[t], nbn[t]);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // flatten: every node -> its root
+    if (w < nT)
+        for (int j = lane; j < s_nb[w]; j += 32) par[w * capb + j] = sfind(par, w * capb + j);
+    __syncthreads();
+    // ---- K3 phase 1, one warp per tile: the non-root bitmap + prefix, the
+    // non-roots per row and the root count of every row.  The first
+    // SMALL_NODES_REG border nodes of the tile are held in registers (lane +
+    // 32 t), and so are the first 32 bitmap words and their prefix (lane =
+    // word): the phases below run on shuffles, with a handful of batched
+    // global round trips (larger tiles take the global fallback).
+    constexpr int NR = 8;  // 256 nodes
+    const int rows_t = w < nT ? tile_rows(g, w) : 0;
+    const int tile = w, nodebase = w * capb, nborder = w < nT ? s_nb[w] : 0;
+    int gcv[NR];
+    bool nonr[NR];
+#pragma unroll
+    for (int t = 0; t < NR; t++) {
+        const int j = 32 * t + lane;
+        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+        nonr[t] = j < nborder && par[nodebase + j] != nodebase + j;
+    }
+    const int32_t *meta = ws.meta + (int64_t)tile * META;
+    const int ncomp = w < nT ? __ldcg(meta + META_NCOMP) : 0;
+    const int rf = w < nT ? __ldcg(meta + META_ROWFIRST + lane) : 0;
+    const int rfx = w < nT ? __ldcg(meta + META_ROWFIRST + (lane + 1 < TH ? lane + 1 : TH)) : 0;
+    const int nbw = (ncomp + 31) >> 5;
+    uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
+    int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(s_pl[w]);  // (the edge list is done): 128 words
+    int32_t *nrow = s_nrp[w];
+    uint32_t bw = 0u;  // bitmap word `lane`
+    int wp = 0;        // its exclusive popcount prefix
+    if (w < nT) {
+        for (int j = lane; j < min(nbw, 128); j += 32) bits[j] = 0u;
+        nrow[lane] = 0;
+        __syncwarp();
+        auto mark = [&](int gc) {
+            const int c = gc & 0xFFFF;
+            if ((c >> 5) < 128) atomicOr(bits + (c >> 5), 1u << (c & 31));
+            else atomicOr(tbits + (c >> 5), 1u << (c & 31));  // (zeroed below: > 4096 components)
+            atomicAdd(nrow + (gc >> 16), 1);
+        };
+        for (int j = 128 + lane; j < nbw; j += 32) tbits[j] = 0u;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < NR; t++)
+            if (nonr[t]) mark(gcv[t]);
+        for (int j = 32 * NR + lane; j < nborder; j += 32)
+            if (par[nodebase + j] != nodebase + j) mark(__ldcg(ws.gnodecomp + nodebase + j));
+        __syncwarp();
+        for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
+            const int j = j0 + lane;
+            const uint32_t bb = j < nbw ? (j < 128 ? bits[j] : __ldcg(tbits + j)) : 0u;
+            uint32_t tot;
+            const int pre = (int)warp_excl_scan(__popc(bb), tot);
+            if (j < nbw) {
+                tbits[j] = bb;
+                twpre[j] = acc + pre;
+            }
+            if (j0 == 0) {
+                bw = bb;
+                wp = pre;
+            }
+            acc += (int)tot;
+        }
+        const int nr = nrow[lane];
+        uint32_t tot;
+        nrow[lane] = (int)warp_excl_scan((uint32_t)nr, tot);  // non-roots in earlier rows
+        const int rfn = lane + 1 < rows_t ? rfx : ncomp;
+        if (lane < rows_t) s_seg[tile * TH + lane] = rfn - rf - nr;
+    }
+    __syncthreads();
+    // ---- K3 phase 2: exclusive scan of the row counts over the whole image
+    {
+        const int v = (int)threadIdx.x < g.H ? s_seg[threadIdx.x] : 0;
+        uint32_t wt;
+        const int pre = (int)warp_excl_scan((uint32_t)v, wt);
+        if (lane == 0) s_wsum[w] = (int)wt;
+        __syncthreads();
+        int off = 0, all = 0;
+        for (int i = 0; i < SMALL_THREADS / 32; i++) {
+            off += i < w ? s_wsum[i] : 0;
+            all += s_wsum[i];
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < g.H) s_seg[threadIdx.x] = off + pre;
+        if (threadIdx.x == 0) n_components[0] = all;
+    }
+    __syncthreads();
+    // non-roots before component c of this warp's tile (bitmap word + prefix)
+    auto nonroots_before = [&](int c) -> int {  // every lane calls it (shuffles)
+        const int wd = c >> 5;
+        uint32_t x = __shfl_sync(FULL, bw, wd & 31);
+        int pre = __shfl_sync(FULL, wp, wd & 31);
+        if (wd >= 32) {
+            x = __ldcg(tbits + wd);
+            pre = __ldcg(twpre + wd);
+        }
+        return pre + __popc(x & ((1u << (c & 31)) - 1u));
+    };
+    // ---- K3 phase 3: label bases of the tile rows and the root nodes' labels
+    const int lb = (lane < rows_t ? s_seg[tile * TH + lane] : 0) + (w < nT ? nrow[lane] : 0) + 1;
+    if (w < nT) {
+        ws.tlb[(int64_t)tile * TH + lane] = lb;
+#pragma unroll
+        for (int t = 0; t < NR; t++) {
+            if (32 * t >= nborder) break;  // warp-uniform
+            const int c = gcv[t] & 0xFFFF, row = gcv[t] >> 16;
+            const int rfr = __shfl_sync(FULL, rf, row), lbr = __shfl_sync(FULL, lb, row);
+            const int nb = nonroots_before(c);
+            const int j = 32 * t + lane;
+            if (j < nborder && !nonr[t]) ws.gnodelab[nodebase + j] = lbr + (c - rfr) - nb;
+        }
+        for (int j0 = 32 * NR; j0 < nborder; j0 += 32) {
+            const int j = j0 + lane;
+            const bool root = j < nborder && par[nodebase + j] == nodebase + j;
+            const int gc = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0, c = gc & 0xFFFF;
+            const int rfr = __shfl_sync(FULL, rf, gc >> 16), lbr = __shfl_sync(FULL, lb, gc >> 16);
+            const int nb = nonroots_before(c);
+            if (root) ws.gnodelab[nodebase + j] = lbr + (c - rfr) - nb;
+        }
+    }
+    __syncthreads();
+    // ---- K4: every non-root border component takes its root's label, at its
+    // slot among the tile's non-roots
+    if (w < nT) {
+        int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
+        int lab[NR];
+#pragma unroll
+        for (int t = 0; t < NR; t++)  // one batch of independent loads
+            lab[t] = nonr[t] ? __ldcg(ws.gnodelab + par[nodebase + 32 * t + lane]) : 0;
+#pragma unroll
+        for (int t = 0; t < NR; t++) {
+            if (32 * t >= nborder) break;  // warp-uniform
+            const int sl = nonroots_before(gcv[t] & 0xFFFF);
+            if (nonr[t]) nrlab[sl] = lab[t];
+        }
+        for (int j0 = 32 * NR; j0 < nborder; j0 += 32) {
+            const int j = j0 + lane;
+            const bool nonroot = j < nborder && par[nodebase + j] != nodebase + j;
+            const int c = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) & 0xFFFF : 0;
+            const int sl = nonroots_before(c);
+            if (nonroot) nrlab[sl] = __ldcg(ws.gnodelab + par[nodebase + j]);
+        }
+    }
+}
+
+// The small-image path (k_small_middle): one image (no batch, no row band),
+// one tile column, at most 32 tile rows, every border node in shared memory.
+static size_t small_smem(const Geometry &g) { return (size_t)g.nT * g.capb * sizeof(int32_t); }
+static bool small_mode(const Geometry &g) {
+    return g.tpi == g.nTy && g.nTx == 1 && g.nT <= SMALL_MAX_TILES && g.H <= SMALL_MAX_ROWS &&
+           small_smem(g) <= 160 * 1024;
+}
+
 // ========================================================================= K5
 // Labeling phase: one warp per 1024-px row segment.  Lane
 // j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
@@ -1513,6 +1798,7 @@ int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a ph
 int pipeline_launches(const Geometry &g) {
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
+    if (small_mode(g)) return 4;  // K1 + its hand-over pass, the fused middle, K5
     return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3, K4, K5, K2 if any edge
 }
 
@@ -1572,6 +1858,9 @@ static cudaError_t set_attrs() {
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))) !=
             cudaSuccess)
             return e;
+    if ((e = cudaFuncSetAttribute(k_small_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)) !=
+        cudaSuccess)
+        return e;
     int dev = 0, sms = 0, per = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
@@ -1598,7 +1887,7 @@ static Geometry with_ptr_alignment(const Geometry &g0, const void *ptr) {
 }
 
 cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8_t *img,
-                            cudaStream_t stream, cudaEvent_t *ev) {
+                            cudaStream_t stream, cudaEvent_t *ev, bool with_border) {
     const Geometry g = with_ptr_alignment(g0, img);
     cudaError_t e = set_attrs();
     if (e != cudaSuccess) return e;
@@ -1631,7 +1920,7 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident / 2), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
     if (e != cudaSuccess) return e;
     mark(K_BORDER);
-    if (g_k1_stop < 99) return cudaGetLastError();
+    if (g_k1_stop < 99 || !with_border) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
     const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
     // few horizontal edges (small images, batches of them): 2 or 4 warps
@@ -1665,6 +1954,16 @@ static cudaError_t launch_write(const Geometry &g0, const Workspace &ws, int32_t
                       g, ws, labels);
 }
 
+// K5 alone (small-image path).  Events (optional): ev[0] before K5, ev[1] after.
+static cudaError_t run_stage_final_write(const Geometry &g, const Workspace &ws, int32_t *labels,
+                                         cudaStream_t stream, cudaEvent_t *ev) {
+    if (ev) cudaEventRecord(ev[0], stream);
+    cudaError_t e = launch_write(g, ws, labels, stream);
+    if (e != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[1], stream);
+    return cudaGetLastError();
+}
+
 // K4 + K5.  Events (optional): ev[0] before K4, ev[1] before K5, ev[2] after.
 cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev) {
@@ -1683,12 +1982,23 @@ cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *lab
 cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *img,
                          int32_t *labels, int32_t *n_components, cudaStream_t stream,
                          cudaEvent_t *ev) {
-    cudaError_t e = run_stage_local(g, ws, img, stream, ev);
+    const bool small = small_mode(g);
+    cudaError_t e = run_stage_local(g, ws, img, stream, ev, !small);
     if (g_k1_stop < 99) {  // development knob: K1 truncated, the rest would read garbage
         for (int i = K_NUMBER; ev && i <= K_COUNT; i++) cudaEventRecord(ev[i], stream);
         return e;
     }
-    if (e == cudaSuccess) e = run_stage_count(g, ws, n_components, stream, ev ? ev + K_NUMBER : nullptr);
+    if (e != cudaSuccess) return e;
+    if (small) {  // K2-K4 fused in one CTA (the event of K2 covers it; K3/K4 spans are empty)
+        e = launch_pdl(k_small_middle, 1, SMALL_THREADS, small_smem(g), stream, g, ws, n_components);
+        if (e != cudaSuccess) return e;
+        if (ev) {
+            cudaEventRecord(ev[K_NUMBER], stream);
+            cudaEventRecord(ev[K_FIXUP], stream);
+        }
+        return run_stage_final_write(g, ws, labels, stream, ev ? ev + K_WRITE : nullptr);
+    }
+    e = run_stage_count(g, ws, n_components, stream, ev ? ev + K_NUMBER : nullptr);
     if (e == cudaSuccess) e = run_stage_final(g, ws, labels, stream, ev ? ev + K_FIXUP : nullptr);
     return e;
 }
