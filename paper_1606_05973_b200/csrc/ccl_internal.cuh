@@ -106,7 +106,7 @@ cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream);
 // Path counters (cumulative over a plan's calls; zeroed by workspace_init):
 // which K1 code paths the tiles took, so tests can prove the dense paths ran.
 enum {
-    STAT_K1_LIST_OVERFLOW = 0,  // k_tile_local tiles whose strip-merge list overflowed (per-row leftover pass)
+    STAT_K1_LIST_OVERFLOW = 0,  // k_tile_local(_wide) tiles whose strip-merge list overflowed (per-row leftover pass)
     STAT_K1_HANDOVER,           // tiles k_tile_local handed to k_tile_big (a row of > 256 runs)
     STAT_K1BIG_LIST_OVERFLOW,   // k_tile_big tiles whose merge list overflowed
     STAT_K1_MERGES,             // strip merges listed (all tiles, both passes)
@@ -156,7 +156,5 @@ cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys,
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
                         int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
                         cudaStream_t stream);
-// Number of kernel launches run_pipeline makes for this geometry.
-int pipeline_launches(const Geometry &g);
 
 }  // namespace cclb

@@ -369,8 +369,9 @@ constexpr int MLCAP = 256;  // P2a -> P2b merge list entries in k_tile_big (4x i
 // array: 6 CTAs/SM).  A tile with a row of more runs (alternating pixels)
 // is left to k_tile_big, which holds the full MAXRUN per row (5 CTAs/SM).
 constexpr int K1_MR = 256;
-template <int MR>
+template <int MR, int MLN = (MR == MAXRUN ? MLCAP : 4 * MLCAP)>
 struct K1SmemT {
+    static constexpr int ML = MLN;  // merge list entries
     uint16_t p[TH * MR];           // parent of each run (the union-find array p of Alg. merge)
     uint32_t bm[TH][WPR];          // run masks (foreground + filled holes)
     // P0: raw foreground; P2a/P2b: upper-side merge heads; P3 on: bitmap of
@@ -383,10 +384,12 @@ struct K1SmemT {
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
     int32_t bcnt[TH];              // border components whose root run lies in the row
-    uint32_t mlist[MR == MAXRUN ? MLCAP : 4 * MLCAP];  // P2a -> P2b: merge pairs (upper | lower << 16)
+    uint32_t mlist[MLN];           // P2a -> P2b: merge pairs (upper | lower << 16)
     int32_t nmerge;
 };
 using K1Smem = K1SmemT<MAXRUN>;
+constexpr int MLWIDE = 2048;  // merge list of the 32-warp K1 (small images: dense tiles, smem to spare)
+using K1SmemWide = K1SmemT<MAXRUN, MLWIDE>;
 
 // Upper-side edges that the copy step does not already cover.  The edge set
 // {(L, leftmost upper run of L)} U {(U, leftmost lower run of U)} connects
@@ -425,7 +428,8 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
                                         const int tile, const int tx, const int ty, int pfd, int pfx, int pfy,
                                         int stop) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    K1SmemT<MR> &sm = *reinterpret_cast<K1SmemT<MR> *>(smem_raw);
+    using Sm = K1SmemT<MR, SR == 1 ? MLWIDE : (MR == MAXRUN ? MLCAP : 4 * MLCAP)>;
+    Sm &sm = *reinterpret_cast<Sm *>(smem_raw);
     auto kidx = [](int r, int o) { return r * MR + o; };
     constexpr int NWK = TH / SR;  // warps of the CTA (SR rows each)
 
@@ -512,7 +516,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // (K5's label stores are evict_first), measured -10 us on C4
     uint64_t pol_last;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-    if (MR < MAXRUN && tile == 0) {  // reset the numbering scan's lookback state (K3)
+    if ((MR < MAXRUN || SR != S) && tile == 0) {  // reset the numbering scan's lookback state (K3)
         for (int i = threadIdx.x; i < g.nTy; i += NWK * 32) ws.scanstate[i] = 0ull;
         if (threadIdx.x == 0) *ws.ticket = 0;
     }
@@ -613,7 +617,7 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         // through in P2b (balanced); what does not fit stays in mc
         if (mc) {
             int idx = atomicAdd(&sm.nmerge, __popc(mc));
-            while (mc && idx < (MR == MAXRUN ? MLCAP : 4 * MLCAP)) {
+            while (mc && idx < Sm::ML) {
                 const int b = __ffs(mc) - 1;
                 const int a = ub + __popc(hu & upto(b)) - 1;         // the upper run with head h
                 const int c = lbase + __popc(hx & ((1u << b) - 1u));  // the lower run containing h-1
@@ -647,10 +651,11 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // many merges no longer holds the barrier); rows whose merges did not fit
     // in the list finish them per lane below.
     const int nmerge = sm.nmerge;
-    constexpr int MLC = MR == MAXRUN ? MLCAP : 4 * MLCAP;
+    constexpr int MLC = Sm::ML;
     if (threadIdx.x == 0 && nmerge > 0) {  // path counters (ccl_plan_counters)
         atomicAdd(ws.stats + STAT_K1_MERGES, (unsigned long long)nmerge);
-        if (nmerge > MLC) atomicAdd(ws.stats + (MR == MAXRUN ? STAT_K1BIG_LIST_OVERFLOW : STAT_K1_LIST_OVERFLOW), 1ull);
+        if (nmerge > MLC)
+            atomicAdd(ws.stats + (MR == MAXRUN && SR == S ? STAT_K1BIG_LIST_OVERFLOW : STAT_K1_LIST_OVERFLOW), 1ull);
     }
     // All 256 threads work through the list at once (union_smem is safe
     // under concurrency, see above).
@@ -840,13 +845,15 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
 
 // Images of few tiles (fewer than the SMs can hold twice over): one warp per
 // tile row, 32 warps per CTA, so a tile's rows are worked on in parallel --
-// the single-image latency of the <= 1 MB regime.
+// the single-image latency of the <= 1 MB regime.  It
+// holds the full MAXRUN runs per row (44 KB), so it never hands a tile over
+// and the hand-over pass is not launched.
 template <bool THR, bool BATCH, bool BANDS = false>
 __global__ void __launch_bounds__(TH * 32, 1)
 k_tile_local_wide(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) {
     pdl_trigger();
     const int tile = blockIdx.x;
-    k1_tile<THR, BATCH, BANDS, K1_MR, 1>(img, g, ws, tile, tile % g.nTx, tile / g.nTx, 0, 0, 0, stop);
+    k1_tile<THR, BATCH, BANDS, MAXRUN, 1>(img, g, ws, tile, tile % g.nTx, tile / g.nTx, 0, 0, 0, stop);
 }
 
 // The tiles k_tile_local handed over (a row with more than K1_MR runs); the
@@ -1292,12 +1299,25 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int nT = g.nT, capb = g.capb;
     if (threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
-    if (threadIdx.x < nT) s_nb[threadIdx.x] = __ldcg(ws.meta + (int64_t)threadIdx.x * META + META_NBORDER);
-    __syncthreads();
-    // the tile's border nodes (only those are ever read), one warp per tile,
-    // four independent loads per lane in flight
+    // per tile (warp w = tile w): its counts and row offsets, the first
+    // SMALL_NODES_REG border nodes' (row, component) in registers (lane + 32 t),
+    // and the parents of its border nodes (only those are ever read) in
+    // shared memory -- all loads of the warp in flight together
+    constexpr int NR = 8;  // 256 nodes in registers
+    const int tile = w, nodebase = w * capb;
+    const int32_t *meta = ws.meta + (int64_t)tile * META;
+    const int nborder = w < nT ? __ldcg(meta + META_NBORDER) : 0;
+    const int ncomp = w < nT ? __ldcg(meta + META_NCOMP) : 0;
+    const int rf = w < nT ? __ldcg(meta + META_ROWFIRST + lane) : 0;
+    const int rfx = w < nT ? __ldcg(meta + META_ROWFIRST + (lane + 1 < TH ? lane + 1 : TH)) : 0;
+    int gcv[NR];
+#pragma unroll
+    for (int t = 0; t < NR; t++) {
+        const int j = 32 * t + lane;
+        gcv[t] = j < min(nborder, capb) && w < nT ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
+    }
+    if (w < nT && lane == 0) s_nb[w] = nborder;
     if (w < nT) {
-        const int nodebase = w * capb, nborder = s_nb[w];
         for (int j0 = 0; j0 < nborder; j0 += 128) {
             int v[4];
 #pragma unroll
@@ -1382,21 +1402,13 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     // 32 t), and so are the first 32 bitmap words and their prefix (lane =
     // word): the phases below run on shuffles, with a handful of batched
     // global round trips (larger tiles take the global fallback).
-    constexpr int NR = 8;  // 256 nodes
     const int rows_t = w < nT ? tile_rows(g, w) : 0;
-    const int tile = w, nodebase = w * capb, nborder = w < nT ? s_nb[w] : 0;
-    int gcv[NR];
     bool nonr[NR];
 #pragma unroll
     for (int t = 0; t < NR; t++) {
         const int j = 32 * t + lane;
-        gcv[t] = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
         nonr[t] = j < nborder && par[nodebase + j] != nodebase + j;
     }
-    const int32_t *meta = ws.meta + (int64_t)tile * META;
-    const int ncomp = w < nT ? __ldcg(meta + META_NCOMP) : 0;
-    const int rf = w < nT ? __ldcg(meta + META_ROWFIRST + lane) : 0;
-    const int rfx = w < nT ? __ldcg(meta + META_ROWFIRST + (lane + 1 < TH ? lane + 1 : TH)) : 0;
     const int nbw = (ncomp + 31) >> 5;
     uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
     int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
@@ -1795,12 +1807,6 @@ __global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, in
 static bool g_attr_done = false;
 int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a phase (timing only)
 
-int pipeline_launches(const Geometry &g) {
-    const int nh = (g.nTy - 1) * g.nTx;
-    const int64_t nv = (int64_t)(g.nTx - 1) * g.H;
-    if (small_mode(g)) return 4;  // K1 + its hand-over pass, the fused middle, K5
-    return 5 + ((nh + (nv + 31) / 32) > 0 ? 1 : 0);  // K1 + its hand-over pass, K3, K4, K5, K2 if any edge
-}
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
 template <typename... KArgs, typename... Args>
@@ -1850,8 +1856,8 @@ static cudaError_t set_attrs() {
     for (auto k : {k_tile_local_wide<false, false>, k_tile_local_wide<true, false>, k_tile_local_wide<false, true>,
                    k_tile_local_wide<true, true>, k_tile_local_wide<false, false, true>,
                    k_tile_local_wide<true, false, true>})
-        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1SmemWide))) !=
+            cudaSuccess)
             return e;
     for (auto k : {k_tile_big<false, false>, k_tile_big<true, false>, k_tile_big<false, true>, k_tile_big<true, true>,
                    k_tile_big<false, false, true>, k_tile_big<true, false, true>})
@@ -1904,7 +1910,7 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
                                                                         : k_tile_local_wide<true, false>)
                         : (batch ? k_tile_local_wide<false, true> : bands ? k_tile_local_wide<false, false, true>
                                                                          : k_tile_local_wide<false, false>);
-        e = launch_pdl(k1, g.nT, TH * 32, sizeof(K1SmemT<K1_MR>), stream, img, g, ws, g_k1_stop);
+        e = launch_pdl(k1, g.nT, TH * 32, sizeof(K1SmemWide), stream, img, g, ws, g_k1_stop);
     } else {
         auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
                         : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
@@ -1914,11 +1920,14 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
                         ws, pfd, pfd % g.nTx, pfd / g.nTx, g_k1_stop);
     }
     if (e != cudaSuccess) return e;
-    auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
-                     : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
-    // a small grid (usually there is nothing to do; its CTAs loop over the list)
-    e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident / 2), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
-    if (e != cudaSuccess) return e;
+    if (!wide) {  // the hand-over pass (the 32-warp K1 holds full rows itself)
+        auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
+                         : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
+        // a small grid (usually there is nothing to do; its CTAs loop over the list)
+        e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident / 2), NW * 32, sizeof(K1Smem), stream, img, g, ws,
+                       g_k1_stop);
+        if (e != cudaSuccess) return e;
+    }
     mark(K_BORDER);
     if (g_k1_stop < 99 || !with_border) return cudaGetLastError();
     const int nh = (g.nTy - 1) * g.nTx;
