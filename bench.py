@@ -430,6 +430,21 @@ def main():
         ms = float(t.item())
     value = H * W / (ms * 1e-3) / 1e9
     result_labels = out.cpu().numpy() if not args.no_parity else None
+
+    # single-call latency: one step with the device idle before it (a
+    # synchronize, then CUDA events around the one call) -- the timed loop
+    # above chains steps back to back (the next step's first kernel is
+    # scheduled while the previous step's last kernel drains)
+    lat = []
+    for _ in range(5):
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        lat.append(a.elapsed_time(b))
+    latency_ms = statistics.median(lat)
     n_gpu = int(n_out.item())
 
     peak, peak_src = peak_hbm()
@@ -457,6 +472,7 @@ def main():
                    "l2": "inputs larger than L2 (466.6 MB image in, 1.87 GB labels out vs 126 MB L2); no flush"},
         "clocks": clk.report(),
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+        "single_call_latency_ms": latency_ms,
         "roofline": roofline,
     }
 
