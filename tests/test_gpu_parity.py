@@ -246,3 +246,34 @@ def test_full_configs_bit_exact(name):
     assert ng == no, (name, ng, no)
     assert np.array_equal(lg, lo), name
     del plan
+
+
+@pytest.mark.parametrize("H,W", [(1024, 1024), (1024, 1000), (1000, 1024), (1025, 1024), (1024, 1025),
+                                 (32, 1024), (33, 1), (1024, 1), (992, 640)])
+def test_small_image_path_limits(H, W):
+    """The small-image path (one tile column, <= 32 tile rows: the 32-warp K1
+    and the single-CTA fused middle) at and just past its limits, on images
+    whose components chain through every tile edge (comb, serpentine) and on
+    dense noise with rows of more than 256 runs (alternating pixels spliced
+    in: the 32-warp K1 holds full rows)."""
+    imgs = [synth.comb(H, W), synth.serpentine(H, W), synth.bernoulli(H, W, 0.6, seed=H + W)]
+    alt = synth.bernoulli(H, W, 0.6, seed=2 * H + W)
+    alt[3::9] = 0
+    alt[3::9, ::2] = 1
+    imgs.append(alt)
+    for k, img in enumerate(imgs):
+        assert_same(img, f"small-path case {k}")
+
+
+def test_small_image_path_thresholded_and_plan_reuse():
+    """Threshold on load and plan reuse through the small-image path."""
+    rng = np.random.default_rng(5)
+    gray = rng.integers(0, 256, size=(700, 900), dtype=np.uint8)
+    plan = ccl.Plan(700, 900)
+    t = torch.from_numpy(gray).cuda()
+    for thr in (0, 64, 127, 200):
+        plan.set_threshold(thr)
+        lab, n = plan.label(t)
+        torch.cuda.synchronize()
+        lo, no = oracle.label((gray > thr).astype(np.uint8))
+        assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo), thr
