@@ -12,5 +12,5 @@ BENCH="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-pari
 timeout 300 $BENCH > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $BENCH > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 300 $BENCH > gpurun_out/plain2_$TAG.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tile_local|k_write|k_border|k_number|k_label|k_fixup' --launch-skip 18 --launch-count 6 -o gpurun_out/prof_$TAG -f $BENCH > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tile_local|k_write|k_border|k_number|k_fixup' --launch-skip 15 --launch-count 5 -o gpurun_out/prof_$TAG -f $BENCH > gpurun_out/ncu_full_$TAG.log 2>&1
 echo done
