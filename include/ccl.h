@@ -258,7 +258,9 @@ ccl_status ccl_nccl_comm_destroy(ccl_nccl_comm_t comm);
  *   ccl_debug_set(1, stop): truncate K1 after phase `stop` (99 = off); the
  *     rest of the pipeline is skipped.  K1 honours it only in builds with
  *     -DCCL_PHASE_KNOB=1 (the checks cost the product kernel ~3 us).  ccl_debug_set(2, x): K1 experiment
- *     bits (1 = no L2 prefetch).  Returns 0, or 1 for an unknown key. */
+ *     bits (1 = no L2 prefetch).  ccl_debug_set(3, 1): no small-image path
+ *     (the general K2-K4 for every image); ccl_debug_set(4, 1): no 32-warp K1.
+ *     Returns 0, or 1 for an unknown key. */
 int ccl_debug_set(int key, int value);
 
 #ifdef __cplusplus

@@ -458,9 +458,11 @@ extern "C" int ccl_debug_workspace(ccl_plan p, void **base, uint64_t *offs, int 
     return A_COUNT;
 }
 
-namespace cclb { extern int g_k1_stop, g_k1_exper; }
+namespace cclb { extern int g_k1_stop, g_k1_exper, g_no_small, g_no_wide; }
 extern "C" int ccl_debug_set(int key, int value) {
     if (key == 1) { cclb::g_k1_stop = value; return 0; }
     if (key == 2) { cclb::g_k1_exper = value; return 0; }
+    if (key == 3) { cclb::g_no_small = value; return 0; }
+    if (key == 4) { cclb::g_no_wide = value; return 0; }
     return 1;
 }

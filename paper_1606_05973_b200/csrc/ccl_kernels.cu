@@ -1227,9 +1227,11 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         const int nodebase = tile * g.capb;
         const int nborder = __ldcg(meta + META_NBORDER);
         const int rf = __ldcg(meta + META_ROWFIRST + lane);
-        const int so = lane < rows ? __ldcg(ws.segoff + (int64_t)(R0 + lane) * g.nTx + tx) : 0;
+        // (segoff, tlb, tbits and twpre were stored by this CTA in phases 1-2:
+        // plain loads after the barrier, not L1-bypassing ones)
+        const int so = lane < rows ? ws.segoff[(int64_t)(R0 + lane) * g.nTx + tx] : 0;
         int32_t *tlb = ws.tlb + (int64_t)tile * TH;
-        const int lb = excl + so + __ldcg(tlb + lane) + 1;
+        const int lb = excl + so + tlb[lane] + 1;
         tlb[lane] = lb;
         const uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
         const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
@@ -1241,7 +1243,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
             const int rfr = __shfl_sync(FULL, rf, row), lbr = __shfl_sync(FULL, lb, row);
             if (root) {
                 const int nrb =
-                    __ldcg(twpre + (c >> 5)) + __popc(__ldcg(tbits + (c >> 5)) & ((1u << (c & 31)) - 1u));
+                    twpre[c >> 5] + __popc(tbits[c >> 5] & ((1u << (c & 31)) - 1u));
                 ws.gnodelab[node] = lbr + (c - rfr) - nrb;
             }
         }
@@ -1294,8 +1296,10 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     __shared__ int32_t s_nrp[SMALL_MAX_TILES][TH];  // non-roots in earlier rows of the tile
     __shared__ int32_t s_wsum[SMALL_THREADS / 32];
     __shared__ uint32_t s_hx[SMALL_MAX_TILES][2][WPR], s_hb[SMALL_MAX_TILES][2][WPR];
-    __shared__ uint32_t s_pl[SMALL_MAX_TILES][128];  // an edge's unions (upper | lower run ordinal << 16)
     int32_t *par = reinterpret_cast<int32_t *>(smem_raw);  // nT * capb node parents
+    // per warp CAPC / 32 words after them: an edge's unions (upper | lower run
+    // ordinal << 16), later the tile's non-root bitmap
+    uint32_t(*s_pl)[CAPC / 32] = reinterpret_cast<uint32_t(*)[CAPC / 32]>(smem_raw + (size_t)g.nT * g.capb * 4);
     const int lane = lane_id(), w = threadIdx.x >> 5;
     const int nT = g.nT, capb = g.capb;
     if (threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
@@ -1392,9 +1396,20 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     __syncthreads();
-    // flatten: every node -> its root
+    // flatten: every node -> its root.  Read-only walks: a halving store by
+    // another thread could otherwise overwrite a node's final root with an
+    // older ancestor after its owner stored the root (that lost labels on
+    // chains through every tile, 1 run in ~30); every store here is a root.
     if (w < nT)
-        for (int j = lane; j < s_nb[w]; j += 32) par[w * capb + j] = sfind(par, w * capb + j);
+        for (int j = lane; j < s_nb[w]; j += 32) {
+            int x = w * capb + j;
+            while (true) {
+                const int px = reinterpret_cast<volatile int32_t *>(par)[x];
+                if (px == x) break;
+                x = px;
+            }
+            par[w * capb + j] = x;
+        }
     __syncthreads();
     // ---- K3 phase 1, one warp per tile: the non-root bitmap + prefix, the
     // non-roots per row and the root count of every row.  The first
@@ -1412,22 +1427,19 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     const int nbw = (ncomp + 31) >> 5;
     uint32_t *tbits = ws.tbits + (int64_t)tile * g.capw;
     int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
-    uint32_t *bits = reinterpret_cast<uint32_t *>(s_pl[w]);  // (the edge list is done): 128 words
+    uint32_t *bits = s_pl[w];  // (the edge list is done): the tile's non-root bitmap
     int32_t *nrow = s_nrp[w];
     uint32_t bw = 0u;  // bitmap word `lane`
     int wp = 0;        // its exclusive popcount prefix
     if (w < nT) {
-        for (int j = lane; j < min(nbw, 128); j += 32) bits[j] = 0u;
+        for (int j = lane; j < nbw; j += 32) bits[j] = 0u;
         nrow[lane] = 0;
         __syncwarp();
         auto mark = [&](int gc) {
             const int c = gc & 0xFFFF;
-            if ((c >> 5) < 128) atomicOr(bits + (c >> 5), 1u << (c & 31));
-            else atomicOr(tbits + (c >> 5), 1u << (c & 31));  // (zeroed below: > 4096 components)
+            atomicOr(bits + (c >> 5), 1u << (c & 31));
             atomicAdd(nrow + (gc >> 16), 1);
         };
-        for (int j = 128 + lane; j < nbw; j += 32) tbits[j] = 0u;
-        __syncwarp();
 #pragma unroll
         for (int t = 0; t < NR; t++)
             if (nonr[t]) mark(gcv[t]);
@@ -1436,7 +1448,7 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         __syncwarp();
         for (int j0 = 0, acc = 0; j0 < nbw; j0 += 32) {
             const int j = j0 + lane;
-            const uint32_t bb = j < nbw ? (j < 128 ? bits[j] : __ldcg(tbits + j)) : 0u;
+            const uint32_t bb = j < nbw ? bits[j] : 0u;
             uint32_t tot;
             const int pre = (int)warp_excl_scan(__popc(bb), tot);
             if (j < nbw) {
@@ -1473,14 +1485,17 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         if (threadIdx.x == 0) n_components[0] = all;
     }
     __syncthreads();
-    // non-roots before component c of this warp's tile (bitmap word + prefix)
+    // non-roots before component c of this warp's tile (bitmap word + prefix;
+    // past the 32 lane-held words, from the shared bitmap)
+    const int pre32 = __shfl_sync(FULL, wp + __popc(bw), 31);  // non-roots in words 0..31
     auto nonroots_before = [&](int c) -> int {  // every lane calls it (shuffles)
         const int wd = c >> 5;
         uint32_t x = __shfl_sync(FULL, bw, wd & 31);
         int pre = __shfl_sync(FULL, wp, wd & 31);
-        if (wd >= 32) {
-            x = __ldcg(tbits + wd);
-            pre = __ldcg(twpre + wd);
+        if (wd >= 32) {  // more than 1024 components in the tile (rare)
+            x = bits[wd];
+            pre = pre32;
+            for (int k = 32; k < wd; k++) pre += __popc(bits[k]);
         }
         return pre + __popc(x & ((1u << (c & 31)) - 1u));
     };
@@ -1495,7 +1510,7 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
             const int rfr = __shfl_sync(FULL, rf, row), lbr = __shfl_sync(FULL, lb, row);
             const int nb = nonroots_before(c);
             const int j = 32 * t + lane;
-            if (j < nborder && !nonr[t]) ws.gnodelab[nodebase + j] = lbr + (c - rfr) - nb;
+            if (j < nborder && !nonr[t]) par[nodebase + j] = ~(lbr + (c - rfr) - nb);  // a root: ~label
         }
         for (int j0 = 32 * NR; j0 < nborder; j0 += 32) {
             const int j = j0 + lane;
@@ -1503,7 +1518,7 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
             const int gc = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) : 0, c = gc & 0xFFFF;
             const int rfr = __shfl_sync(FULL, rf, gc >> 16), lbr = __shfl_sync(FULL, lb, gc >> 16);
             const int nb = nonroots_before(c);
-            if (root) ws.gnodelab[nodebase + j] = lbr + (c - rfr) - nb;
+            if (root) par[nodebase + j] = ~(lbr + (c - rfr) - nb);
         }
     }
     __syncthreads();
@@ -1514,7 +1529,7 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         int lab[NR];
 #pragma unroll
         for (int t = 0; t < NR; t++)  // one batch of independent loads
-            lab[t] = nonr[t] ? __ldcg(ws.gnodelab + par[nodebase + 32 * t + lane]) : 0;
+            lab[t] = nonr[t] ? ~par[par[nodebase + 32 * t + lane]] : 0;  // the root's ~label
 #pragma unroll
         for (int t = 0; t < NR; t++) {
             if (32 * t >= nborder) break;  // warp-uniform
@@ -1523,20 +1538,25 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         }
         for (int j0 = 32 * NR; j0 < nborder; j0 += 32) {
             const int j = j0 + lane;
-            const bool nonroot = j < nborder && par[nodebase + j] != nodebase + j;
+            const int pj = j < nborder ? par[nodebase + j] : 0;
+            const bool nonroot = j < nborder && pj >= 0 && pj != nodebase + j;  // (roots hold ~label < 0)
             const int c = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) & 0xFFFF : 0;
             const int sl = nonroots_before(c);
-            if (nonroot) nrlab[sl] = __ldcg(ws.gnodelab + par[nodebase + j]);
+            if (nonroot) nrlab[sl] = ~par[pj];
         }
     }
 }
 
 // The small-image path (k_small_middle): one image (no batch, no row band),
 // one tile column, at most 32 tile rows, every border node in shared memory.
-static size_t small_smem(const Geometry &g) { return (size_t)g.nT * g.capb * sizeof(int32_t); }
+constexpr size_t SMALL_SMEM_MAX = 190 * 1024;  // dynamic; + ≈ 25 KB static < 227 KB
+static size_t small_smem(const Geometry &g) {
+    return (size_t)g.nT * g.capb * sizeof(int32_t) + (size_t)SMALL_MAX_TILES * (CAPC / 32) * sizeof(uint32_t);
+}
+extern int g_no_small;
 static bool small_mode(const Geometry &g) {
-    return g.tpi == g.nTy && g.nTx == 1 && g.nT <= SMALL_MAX_TILES && g.H <= SMALL_MAX_ROWS &&
-           small_smem(g) <= 160 * 1024;
+    return !g_no_small && g.tpi == g.nTy && g.nTx == 1 && g.nT <= SMALL_MAX_TILES && g.H <= SMALL_MAX_ROWS &&
+           small_smem(g) <= SMALL_SMEM_MAX;
 }
 
 // ========================================================================= K5
@@ -1545,7 +1565,7 @@ static bool small_mode(const Geometry &g) {
 // warp is one contiguous 512-byte stretch of the output row.
 constexpr int K5_WARPS = 16;  // measured vs 4 and 8
 __global__ void __launch_bounds__(K5_WARPS * 32, 4)
-k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
+k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, int mshift) {
     pdl_trigger();
     pdl_wait();
     // s_lab[w][1 + k] = final label of run k of warp w's row (entry 0 and the
@@ -1558,7 +1578,9 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
     // stretch of the label image
     const uint32_t seg = blockIdx.x * K5_WARPS + wi;  // (row, tile column); nseg < 2^31
     if (seg >= (uint32_t)g.nseg) return;
-    const int row = (int)(seg / (uint32_t)g.nTx), tx = (int)(seg - (uint32_t)row * (uint32_t)g.nTx);
+    // seg / nTx by the host's magic multiplier (exact for seg < 2^31; m = 0: nTx = 1)
+    const int row = magic ? (int)(__umulhi(seg, magic) >> mshift) : (int)seg;
+    const int tx = (int)(seg - (uint32_t)row * (uint32_t)g.nTx);
     const int ty = row_tile(g, row);
     const int C0 = tx * TW, tile = ty * g.nTx + tx;
     const int vcols = min(TW, g.W - C0);
@@ -1598,9 +1620,11 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
             const int c = __shfl_sync(FULL, rfv, row) + rank, wd = c >> 5;
             uint32_t w = __shfl_sync(FULL, bwv, wd & 31);
             int pre = __shfl_sync(FULL, wpv, wd & 31);
-            if (wd >= 32) {  // more than 1024 components in the tile
-                w = __ldcg(tbits + wd);
-                pre = __ldcg(twpre + wd);
+            if (__any_sync(FULL, wd >= 32)) {  // warp-uniform: more than 1024 components in the tile
+                if (wd >= 32) {
+                    w = __ldcg(tbits + wd);
+                    pre = __ldcg(twpre + wd);
+                }
             }
             const int nb = pre + __popc(w & ((1u << (c & 31)) - 1u));
             const int lb = __shfl_sync(FULL, lbv, row);
@@ -1608,7 +1632,9 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels) {
             int lab = lb + rank - nb;
             if (__any_sync(FULL, nonroot)) {  // warp-uniform: most chunks have no merged border component
                 const int nla = __shfl_sync(FULL, nlv, nb & 31), nlb = __shfl_sync(FULL, nlv2, nb & 31);
-                if (nonroot) lab = nb < 32 ? nla : (nb < 64 ? nlb : __ldcg(nrlab + nb));
+                if (nonroot) lab = nb < 32 ? nla : nlb;
+                if (__any_sync(FULL, nonroot && nb >= 64))  // warp-uniform: more than 64 non-roots
+                    if (nonroot && nb >= 64) lab = __ldcg(nrlab + nb);
             }
             return lab + off;
         };
@@ -1805,7 +1831,8 @@ __global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, in
 
 // ==================================================================== host
 static bool g_attr_done = false;
-int g_k1_stop = 99, g_k1_exper = 0;  // development knob: truncate K1 after a phase (timing only)
+int g_k1_stop = 99, g_k1_exper = 0;
+int g_no_small = 0, g_no_wide = 0;  // development knobs: force the general middle / the 8-warp K1  // development knob: truncate K1 after a phase (timing only)
 
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
@@ -1864,7 +1891,7 @@ static cudaError_t set_attrs() {
         if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K1Smem))) !=
             cudaSuccess)
             return e;
-    if ((e = cudaFuncSetAttribute(k_small_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)) !=
+    if ((e = cudaFuncSetAttribute(k_small_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM_MAX)) !=
         cudaSuccess)
         return e;
     int dev = 0, sms = 0, per = 0;
@@ -1904,7 +1931,7 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     const bool batch = g.tpi != g.nTy, bands = ws.boff != nullptr;  // (a band workspace has its offset)
     // few tiles: the 32-warp K1 (one warp per tile row) shortens the tile's
     // latency; many tiles: the 8-warp K1 (6 CTAs per SM) keeps the SMs busy
-    const bool wide = g.nT * 4 <= g_k1_resident;
+    const bool wide = !g_no_wide && g.nT * 4 <= g_k1_resident;
     if (wide) {
         auto k1 = g.thr ? (batch ? k_tile_local_wide<true, true> : bands ? k_tile_local_wide<true, false, true>
                                                                         : k_tile_local_wide<true, false>)
@@ -1957,10 +1984,29 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
     return cudaGetLastError();
 }
 
+// Magic multiplier for n / d with n < 2^31 (Granlund-Montgomery, N = 31
+// bits): l = ceil(log2 d), m = ceil(2^(31+l) / d) < 2^32, and n / d =
+// umulhi(n, m) >> (l - 1) for every n < 2^31 (d >= 2; checked exhaustively
+// for d < 5000 and at the powers of two).  d = 1 is special-cased (m = 0).
+static void magic_u32(uint32_t d, uint32_t *m, int *s) {
+    if (d < 2) {
+        *m = 0;
+        *s = 0;
+        return;
+    }
+    int l = 0;
+    while ((1u << l) < d) l++;
+    *m = (uint32_t)((((uint64_t)1 << (31 + l)) + d - 1) / d);
+    *s = l - 1;
+}
+
 static cudaError_t launch_write(const Geometry &g0, const Workspace &ws, int32_t *labels, cudaStream_t stream) {
     const Geometry g = with_ptr_alignment(g0, labels);
+    uint32_t magic;
+    int mshift;
+    magic_u32((uint32_t)g.nTx, &magic, &mshift);
     return launch_pdl(k_write, (unsigned)(((int64_t)g.nseg + K5_WARPS - 1) / K5_WARPS), K5_WARPS * 32, 0, stream,
-                      g, ws, labels);
+                      g, ws, labels, magic, mshift);
 }
 
 // K5 alone (small-image path).  Events (optional): ev[0] before K5, ev[1] after.

@@ -97,6 +97,27 @@ def test_concurrent_union_paths_bit_exact(case):
     assert not bad, f"{case}: runs {bad[:10]} of {reps} differ from the oracle ({c})"
 
 
+def test_small_path_chains_repeated():
+    """The small-image path's fused middle (one CTA; unions, flatten and labels
+    in shared memory) on images whose one component chains through every tile
+    (serpentine, comb) and dense noise, 60 runs each, every run bit-exact.  (A
+    flatten that let another thread's path-halving store overwrite a node's
+    final root lost labels in ~1 run of 30 before it was made read-only.)"""
+    cases = []
+    for (H, W) in [(1024, 1024), (1024, 1000), (1024, 1), (992, 640)]:
+        cases += [synth.serpentine(H, W), synth.comb(H, W), synth.bernoulli(H, W, 0.6, seed=H + W)]
+    for img in cases:
+        lo, no = oracle.label(img)
+        ref = torch.from_numpy(lo).cuda()
+        t = torch.from_numpy(img).cuda()
+        bad = 0
+        for _ in range(60):
+            lab, n = ccl.label(t)
+            torch.cuda.synchronize()
+            bad += int(int(n.item()) != no or not torch.equal(lab, ref))
+        assert bad == 0, (img.shape, bad)
+
+
 def test_unaligned_base_pointers():
     """W % 16 == 0 but img / labels base pointers off 16-byte alignment: the
     kernels must take the narrow paths (no misaligned vector access)."""
