@@ -177,7 +177,7 @@ def make_roofline(ktimes, H, W, bh, ms, ws, peak, peak_src, workload):
          "frac": d.get("frac", 0.0), "traffic": d.get("ncu_dram_bytes"),
          "algorithmic_bytes_per_launch": d.get("algorithmic_bytes", 0),
          "peak_source": peak_src,
-         "path": {"achieved": ach_gpu, "frac": ach_gpu / peak,
+         "path": {"achieved": ach_gpu, "frac": ach_gpu / peak, "frac_of_8tbps": ach_gpu / 8000.0,
                   "algorithmic_bytes_per_step": alg // ws if ws > 1 else alg,
                   "per_gpu": ws > 1,
                   "traffic": sum(tr_all) if tr_all and all(t is not None for t in tr_all) else None},
