@@ -1292,7 +1292,6 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     pdl_wait();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ int32_t s_seg[SMALL_MAX_ROWS];       // root count per image row, then its exclusive prefix
-    __shared__ int32_t s_nb[SMALL_MAX_TILES];       // border nodes per tile
     __shared__ int32_t s_nrp[SMALL_MAX_TILES][TH];  // non-roots in earlier rows of the tile
     __shared__ int32_t s_wsum[SMALL_THREADS / 32];
     __shared__ uint32_t s_hx[SMALL_MAX_TILES][2][WPR], s_hb[SMALL_MAX_TILES][2][WPR];
@@ -1320,7 +1319,6 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         const int j = 32 * t + lane;
         gcv[t] = j < min(nborder, capb) && w < nT ? __ldcg(ws.gnodecomp + nodebase + j) : 0;
     }
-    if (w < nT && lane == 0) s_nb[w] = nborder;
     if (w < nT) {
         for (int j0 = 0; j0 < nborder; j0 += 128) {
             int v[4];
@@ -1396,21 +1394,8 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     __syncthreads();
-    // flatten: every node -> its root.  Read-only walks: a halving store by
-    // another thread could otherwise overwrite a node's final root with an
-    // older ancestor after its owner stored the root (that lost labels on
-    // chains through every tile, 1 run in ~30); every store here is a root.
-    if (w < nT)
-        for (int j = lane; j < s_nb[w]; j += 32) {
-            int x = w * capb + j;
-            while (true) {
-                const int px = reinterpret_cast<volatile int32_t *>(par)[x];
-                if (px == x) break;
-                x = px;
-            }
-            par[w * capb + j] = x;
-        }
-    __syncthreads();
+    // (no flatten: the root test needs no more than par[x] == x, and K4
+    // below walks each non-root up to its root, read-only)
     // ---- K3 phase 1, one warp per tile: the non-root bitmap + prefix, the
     // non-roots per row and the root count of every row.  The first
     // SMALL_NODES_REG border nodes of the tile are held in registers (lane +
@@ -1526,10 +1511,19 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
     // slot among the tile's non-roots
     if (w < nT) {
         int32_t *nrlab = ws.nrlab + (int64_t)tile * g.capc;
+        // a root holds ~label (< 0) since phase 3, every other node a parent
+        // (>= 0): walk read-only up to the root (no store may leave a node
+        // pointing below its root -- see DESIGN.md "Small images")
+        auto root_label = [&](int y) -> int {
+            while (true) {
+                const int v = reinterpret_cast<volatile int32_t *>(par)[y];
+                if (v < 0) return ~v;
+                y = v;
+            }
+        };
         int lab[NR];
 #pragma unroll
-        for (int t = 0; t < NR; t++)  // one batch of independent loads
-            lab[t] = nonr[t] ? ~par[par[nodebase + 32 * t + lane]] : 0;  // the root's ~label
+        for (int t = 0; t < NR; t++) lab[t] = nonr[t] ? root_label(par[nodebase + 32 * t + lane]) : 0;
 #pragma unroll
         for (int t = 0; t < NR; t++) {
             if (32 * t >= nborder) break;  // warp-uniform
@@ -1539,10 +1533,10 @@ k_small_middle(Geometry g, Workspace ws, int32_t *n_components) {
         for (int j0 = 32 * NR; j0 < nborder; j0 += 32) {
             const int j = j0 + lane;
             const int pj = j < nborder ? par[nodebase + j] : 0;
-            const bool nonroot = j < nborder && pj >= 0 && pj != nodebase + j;  // (roots hold ~label < 0)
+            const bool nonroot = j < nborder && pj >= 0;  // (roots hold ~label < 0)
             const int c = j < nborder ? __ldcg(ws.gnodecomp + nodebase + j) & 0xFFFF : 0;
             const int sl = nonroots_before(c);
-            if (nonroot) nrlab[sl] = ~par[pj];
+            if (nonroot) nrlab[sl] = root_label(pj);
         }
     }
 }
@@ -1638,7 +1632,9 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
             }
             return lab + off;
         };
-        const int l0 = run_label(rc0);
+        // (entries past the row's runs are stale workspace: never use them,
+        // their decoded indices could point past the tile's tables)
+        const int l0 = run_label(lane < (int)nr ? rc0 : 0u);
         if (lane < (int)nr) rowlab[lane] = l0;
 #pragma unroll 1
         for (int k0 = 32; k0 < (int)nr; k0 += 32) {  // warp-uniform: the shuffles need every lane
