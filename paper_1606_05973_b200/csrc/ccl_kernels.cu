@@ -627,17 +627,23 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         }
         sm.mc[rl][lane] = mc;
         const bool instrip = i > 0;
-        // upper heads of this word and the next word's first pixel, so the
-        // run of the upper pixel q in [-1, 32] is ub - 1 + (heads at <= q)
-        const uint64_t hu64 = (uint64_t)hu | ((uint64_t)(hun & 1u) << 32);
-        const uint32_t uLu = uL | u;
+        // The run of the leftmost upper foreground pixel q among b-1, b, b+1
+        // is ub - 1 + (upper heads at <= q).  Heads at <= q = heads at <= b+1
+        // less the head at b+1 when q = b-1 (q = b-1 rules out a head at b,
+        // q = b one at b+1), so with hnext (bit b = upper head at b+1; bit 31
+        // the next word's first pixel) and hb (q = b-1 and a head at b+1) the
+        // count is (hu & 1) + popc(hnext & bits 0..b) - hb[b]: two popcounts
+        // and three-input logic per touch, no 64-bit or variable shifts.
+        const uint32_t hnext = (hu >> 1) | (lane == 31 ? 0u : hun << 31);  // no word right of the tile
+        const uint32_t hb = uL & hnext;
+        const int ubc = ub - 1 + (int)(hu & 1u);
         while (ft) {
-            const int b = __ffs(ft) - 1;
-            ft &= ft - 1;
-            // leftmost upper foreground pixel q among p-1, p, p+1 (q+1 = b, b+1, b+2)
-            const int q1 = b + 2 - (int)((uL >> b) & 1u) - (int)((uLu >> b) & 1u);
-            const int ui = ub - 1 + __popcll(hu64 & ((1ull << q1) - 1ull));
-            vp[lbase + __popc(hx & upto(b))] = instrip ? vp[ui] : (uint16_t)ui;
+            const uint32_t f1 = ft - 1u;
+            const uint32_t m = ft ^ f1;              // bits 0..b, b = lowest touch
+            const uint32_t xb = hb & ft & ~f1;       // bit b if q = b-1 skips a head at b+1
+            ft &= f1;
+            const int ui = ubc + __popc(hnext & (m ^ xb));
+            vp[lbase + __popc(hx & m)] = instrip ? vp[ui] : (uint16_t)ui;
         }
         __syncwarp();
     }
@@ -825,7 +831,10 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
 }
 
 template <bool THR, bool BATCH, bool BANDS = false>
-__global__ void __launch_bounds__(NW * 32, 6)
+#ifndef K1_MINB
+#define K1_MINB 6  // CTAs per SM (40 registers; 7 forces 32 and spills)
+#endif
+__global__ void __launch_bounds__(NW * 32, K1_MINB)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int pfx, int pfy, int stop) {
     pdl_trigger();
     // a 2-D grid (tile columns x tile rows; CTAs still start in raster
@@ -1611,7 +1620,10 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
         // Every lane runs the shuffles (entries past the row are harmless).
         auto run_label = [&](uint32_t v) -> int {
             const int row = (int)(v >> 9) & 31, rank = (int)(v & 0x1FFu);
-            const int c = __shfl_sync(FULL, rfv, row) + rank, wd = c >> 5;
+            // (clamped: an entry past the row's runs is stale workspace and
+            // decodes to anything; its label is never stored, but its loads
+            // must stay inside the tile's tables)
+            const int c = min(__shfl_sync(FULL, rfv, row) + rank, g.capc - 1), wd = c >> 5;
             uint32_t w = __shfl_sync(FULL, bwv, wd & 31);
             int pre = __shfl_sync(FULL, wpv, wd & 31);
             if (__any_sync(FULL, wd >= 32)) {  // warp-uniform: more than 1024 components in the tile
@@ -1628,13 +1640,13 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
                 const int nla = __shfl_sync(FULL, nlv, nb & 31), nlb = __shfl_sync(FULL, nlv2, nb & 31);
                 if (nonroot) lab = nb < 32 ? nla : nlb;
                 if (__any_sync(FULL, nonroot && nb >= 64))  // warp-uniform: more than 64 non-roots
-                    if (nonroot && nb >= 64) lab = __ldcg(nrlab + nb);
+                    if (nonroot && nb >= 64) lab = __ldcg(nrlab + min((uint32_t)nb, (uint32_t)g.capc - 1u));
             }
             return lab + off;
         };
-        // (entries past the row's runs are stale workspace: never use them,
-        // their decoded indices could point past the tile's tables)
-        const int l0 = run_label(lane < (int)nr ? rc0 : 0u);
+        // (entries past the row's runs are decoded too -- clamped, see
+        // run_label -- so the shuffles do not wait for the run count)
+        const int l0 = run_label(rc0);
         if (lane < (int)nr) rowlab[lane] = l0;
 #pragma unroll 1
         for (int k0 = 32; k0 < (int)nr; k0 += 32) {  // warp-uniform: the shuffles need every lane
