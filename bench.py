@@ -292,7 +292,18 @@ def small_images(dev, stream, batch=64, reps=20):
             b.record(stream)
             torch.cuda.synchronize(dev)
             ms = a.elapsed_time(b) / reps
-            out[tag] = {"us_per_call": ms * 1e3, "gpx_s": px / (ms * 1e-3) / 1e9}
+            # us_per_call: back-to-back calls (each call's launch overlaps
+            # the previous call's tail); isolated_us: one call between two
+            # synchronisations (median of reps), the latency a lone call sees
+            iso = []
+            for _ in range(reps):
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                iso.append(a.elapsed_time(b) * 1e3)
+            out[tag] = {"us_per_call": ms * 1e3, "gpx_s": px / (ms * 1e-3) / 1e9,
+                        "isolated_us": statistics.median(iso)}
         res[name] = out
     return res
 

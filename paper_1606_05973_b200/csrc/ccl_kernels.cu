@@ -755,10 +755,12 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     const int ncomp = (int)rtot, nborder = (int)btot;
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
+    const int64_t dstride = (int64_t)g.nTx * g.maxrun;
+    uint16_t *dst = ws.runcomp + ((int64_t)(R0 + r0) * g.nTx + tx) * g.maxrun - dstride;
 #pragma unroll 1
     for (int i = 0; i < SR; i++) {
         const int rl = r0 + i, n = sm.nrun[rl];
-        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + rl) * g.nTx + tx) * g.maxrun;
+        dst += dstride;
         int bi = __shfl_sync(FULL, bfirst, rl);
         const int rf = __shfl_sync(FULL, rowfirst, rl);
         const bool hasb = sm.bcnt[rl] != 0;
