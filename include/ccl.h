@@ -260,6 +260,9 @@ ccl_status ccl_nccl_comm_destroy(ccl_nccl_comm_t comm);
  *     -DCCL_PHASE_KNOB=1 (the checks cost the product kernel ~3 us).  ccl_debug_set(2, x): K1 experiment
  *     bits (1 = no L2 prefetch).  ccl_debug_set(3, 1): no small-image path
  *     (the general K2-K4 for every image); ccl_debug_set(4, 1): no 32-warp K1.
+ *     ccl_debug_set(5, seed): workspaces created from now on (plans,
+ *     one-shot calls) are filled with pseudo-random words (0 = off), so tests
+ *     can check that no kernel reads workspace this call has not written.
  *     Returns 0, or 1 for an unknown key. */
 int ccl_debug_set(int key, int value);
 

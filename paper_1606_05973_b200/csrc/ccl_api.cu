@@ -112,6 +112,23 @@ Workspace workspace_bind(const Geometry &g, void *base) {
     return w;
 }
 
+// Test hook (ccl_debug_set(5, seed)): fresh workspaces are filled with
+// pseudo-random words instead of whatever the allocation held, so tests can
+// check that no kernel decodes workspace it has not written in this call.
+static uint32_t g_poison = 0;
+__global__ void k_poison(uint32_t *p, size_t n, uint32_t seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 0x9E3779B9u ^ seed;
+        h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+        p[i] = h;
+    }
+}
+cudaError_t workspace_poison(void *mem, size_t bytes, cudaStream_t s) {
+    if (!g_poison) return cudaSuccess;
+    k_poison<<<1184, 256, 0, s>>>(static_cast<uint32_t *>(mem), bytes / 4, g_poison);
+    return cudaGetLastError();
+}
+
 cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream) {
     cudaError_t e = cudaMemsetAsync(ws.k1over_n, 0, sizeof(int32_t), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(ws.stats, 0, STAT_COUNT * sizeof(unsigned long long), stream);
@@ -225,7 +242,8 @@ static ccl_status label_oneshot(const uint8_t *img, int B, int H, int W, int thr
     if (e == cudaErrorMemoryAllocation) return CCL_OUT_OF_MEMORY;
     if (e != cudaSuccess) return CCL_CUDA_ERROR;
     Workspace ws = workspace_bind(g, mem);
-    e = workspace_init(ws, s);
+    e = workspace_poison(mem, total, s);
+    if (e == cudaSuccess) e = workspace_init(ws, s);
     if (e == cudaSuccess) e = run_pipeline(g, ws, img, labels, n_components, s, nullptr);
     cudaError_t e2 = cudaFreeAsync(mem, s);
     if (e != cudaSuccess || e2 != cudaSuccess) return CCL_CUDA_ERROR;
@@ -254,7 +272,8 @@ ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out) {
         return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
     }
     p->ws = workspace_bind(p->g, p->ws_mem);
-    if (workspace_init(p->ws, 0) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+    if (workspace_poison(p->ws_mem, p->ws_bytes, 0) != cudaSuccess || workspace_init(p->ws, 0) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
         cudaFree(p->ws_mem);
         delete p;
         return CCL_CUDA_ERROR;
@@ -464,5 +483,6 @@ extern "C" int ccl_debug_set(int key, int value) {
     if (key == 2) { cclb::g_k1_exper = value; return 0; }
     if (key == 3) { cclb::g_no_small = value; return 0; }
     if (key == 4) { cclb::g_no_wide = value; return 0; }
+    if (key == 5) { cclb::g_poison = (uint32_t)value; return 0; }
     return 1;
 }

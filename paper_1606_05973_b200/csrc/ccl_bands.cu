@@ -160,6 +160,7 @@ ccl_status band_init(Band &b, int band_H, int W, int row0) {
     workspace_layout(b.g, offs, &total);
     CK(cudaMalloc(&b.mem, total));
     b.ws = workspace_bind(b.g, b.mem);
+    CK(workspace_poison(b.mem, total, 0));
     CK(workspace_init(b.ws, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMalloc(&b.d_nodes, sizeof(int32_t) * 2 * W));

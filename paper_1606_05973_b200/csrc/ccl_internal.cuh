@@ -101,6 +101,8 @@ void workspace_layout(const Geometry &g, size_t offs[], size_t *total);
 Workspace workspace_bind(const Geometry &g, void *base);
 // Zeroes the counters a new workspace must start with (before its first call).
 cudaError_t workspace_init(const Workspace &ws, cudaStream_t stream);
+// test hook ccl_debug_set(5, seed): fill a fresh workspace with pseudo-random words
+cudaError_t workspace_poison(void *mem, size_t bytes, cudaStream_t stream);
 
 
 // Path counters (cumulative over a plan's calls; zeroed by workspace_init):

@@ -3,7 +3,9 @@ recipes through every entry point (one-shot, plan, threshold, batch, row
 bands on one GPU), each output compared with the oracle bit for bit.  Plans
 and one-shot workspaces are recycled device memory, so stale workspace
 contents get exercised too.
-usage: [FUZZ_TRACE=1] python scripts/fuzz.py [seconds] [seed]"""
+With FUZZ_POISON=seed every fresh workspace is filled with pseudo-random
+words first (test hook ccl_debug_set(5, seed)).
+usage: [FUZZ_TRACE=1] [FUZZ_POISON=seed] python scripts/fuzz.py [seconds] [seed]"""
 import ctypes
 import os
 import sys
@@ -20,6 +22,9 @@ import synth
 _cud = ctypes.CDLL("libcudart.so.12")
 _cud.cudaGetErrorString.restype = ctypes.c_char_p
 
+if os.environ.get("FUZZ_POISON"):
+    ccl._L.ccl_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
+    ccl._L.ccl_debug_set(5, int(os.environ["FUZZ_POISON"]))
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
 recipes = list(synth.CONFIGS)

@@ -277,3 +277,43 @@ def test_small_image_path_thresholded_and_plan_reuse():
         torch.cuda.synchronize()
         lo, no = oracle.label((gray > thr).astype(np.uint8))
         assert int(n.item()) == no and np.array_equal(lab.cpu().numpy(), lo), thr
+
+
+def test_poisoned_and_recycled_workspace():
+    """No kernel may read workspace this call has not written.  Fresh plan
+    and one-shot workspaces are filled with pseudo-random words (test hook
+    ccl_debug_set(5, seed)), then labeled in alternating shapes and densities
+    (one-shot workspaces also come back from the stream-ordered pool holding
+    the previous geometry's tables).  K5 decodes run entries past a row's
+    runs too, clamped into the tile's tables: the randomised fuzz
+    (scripts/fuzz.py) found an illegal address there on narrow images."""
+    import ctypes
+    ccl._L.ccl_debug_set.argtypes = [ctypes.c_int, ctypes.c_int]
+    cases = [(2000, 3000, 0.5), (700, 5000, 0.05), (32, 56, 0.5), (1500, 2100, 0.6), (274, 965, 0.2),
+             (3000, 1100, 0.02), (33, 56, 0.8), (64, 4100, 0.45), (64, 56, 0.5), (31, 56, 0.2), (512, 512, 0.5)]
+    imgs = [synth.bernoulli(H, W, p, seed=11 + i) for i, (H, W, p) in enumerate(cases)]
+    refs = [oracle.label(im) for im in imgs]
+    stack = np.stack([synth.bernoulli(40, 56, p, seed=5) for p in (0.2, 0.5, 0.8)])
+    srefs = [oracle.label(im) for im in stack]
+    try:
+        for seed in (0x9E3779B9, 12345, 0x7FFFFFFF):
+            assert ccl._L.ccl_debug_set(5, seed) == 0
+            for im, (lo, no) in zip(imgs, refs):
+                for plan in (None, ccl.Plan(*im.shape)):
+                    lg, ng = gpu_label(im, plan)
+                    assert ng == no and np.array_equal(lg, lo), (im.shape, seed, plan is None)
+            # a batch of three (tile rows per image) and the threshold path
+            lab, n = ccl.label_batch(torch.from_numpy(stack).cuda())
+            torch.cuda.synchronize()
+            for b in range(len(stack)):
+                assert int(n[b].item()) == srefs[b][1] and np.array_equal(lab[b].cpu().numpy(), srefs[b][0])
+            for k, nb in ((0, 3), (4, 5), (9, 2)):  # row bands on one GPU (their own workspaces)
+                lab, n = ccl.label_banded(torch.from_numpy(imgs[k]).cuda(), nb)
+                torch.cuda.synchronize()
+                assert int(n.item()) == refs[k][1] and np.array_equal(lab.cpu().numpy(), refs[k][0]), (k, nb)
+            gray = (imgs[4] * 200).astype(np.uint8)
+            lab, n = ccl.label(torch.from_numpy(gray).cuda(), threshold=100)
+            torch.cuda.synchronize()
+            assert int(n.item()) == refs[4][1] and np.array_equal(lab.cpu().numpy(), refs[4][0])
+    finally:
+        ccl._L.ccl_debug_set(5, 0)
