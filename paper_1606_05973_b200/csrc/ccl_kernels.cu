@@ -473,6 +473,21 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         if ((int)(threadIdx.x >> 3) < rows && pcol < g.W)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(img + (int64_t)prow * g.W + pcol));
     }
+    // Every run starts as its own label: the warp's rows
+    // are one contiguous range of p, set to the identity with 16-byte stores
+    // (8 entries each; entries past a row's runs are never read) before the
+    // grid dependency wait -- shared memory only.
+    {
+        constexpr int NV = SR * MR / 8;  // uint4 per warp
+        static_assert(NV % 32 == 0, "p init: whole uint4 per lane");
+        uint4 *pv = reinterpret_cast<uint4 *>(sm.p + kidx(r0, 0));
+        const uint32_t e0 = (uint32_t)kidx(r0, 0);
+#pragma unroll
+        for (int v = lane; v < NV; v += 32) {
+            const uint32_t w0 = (e0 + 8u * v) * 0x10001u + 0x10000u;  // entries e, e+1
+            pv[v] = make_uint4(w0, w0 + 0x20002u, w0 + 0x40004u, w0 + 0x60006u);
+        }
+    }
     // The image may be written by the kernel just before this one on the
     // stream (the caller's producer): no pixel is loaded before the wait.
     pdl_wait();
@@ -537,8 +552,8 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     // foreground).  Only holes whose neighbours lie in
     // this tile are filled: any subset of bridged holes preserves the
     // partition of the foreground, and K2/K5 read the same run mask.
-    // Then run heads, per-word run counts, and every run starts as its own
-    // label.
+    // Then run heads and per-word run counts (p was set to the identity
+    // above).
     bool over = false;  // a row of this warp has more runs than the p array holds
 #pragma unroll
     for (int i = 0; i < SR; i++) {
@@ -558,11 +573,6 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         sm.hbase[rl][lane] = (uint16_t)base;
         if (lane == 0) sm.nrun[rl] = (int)nr;
         over |= (int)nr > MR;
-#pragma unroll 1
-        for (int o = 2 * lane; o < min((int)nr, MR); o += 64) {  // two runs per 32-bit store
-            const uint32_t k = (uint32_t)kidx(rl, o);
-            reinterpret_cast<volatile uint32_t *>(vp)[k >> 1] = k | ((k + 1) << 16);
-        }
     }
     if (MR < MAXRUN) {
         if (__syncthreads_or(over)) {  // too many runs in a row: k_tile_big takes the tile
@@ -602,11 +612,20 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         const uint32_t hun = __shfl_down_sync(FULL, hu, 1);
         const uint32_t uL = (u << 1) | (up >> 31);  // upper pixel at p-1
         const uint32_t t = x & (u | uL | (u >> 1) | (un << 31));
-        const uint32_t s = smear_up(t, x);
-        const uint32_t cin = carry_in_fwd(((x >> 31) & (s >> 31)) != 0, x == FULL) & x & 1u;
+        // First touch of every run and S_ = the run pixels at or after it,
+        // by one addition: q = untouched run pixels; adding the untouched run
+        // heads (bit 0 counts as a head while the run from the left lanes has
+        // no touch yet) carries through each head's untouched prefix P and
+        // stops at the first touch.  Across lanes: a carry-lookahead on
+        // "touched by bit 31" through all-ones words (tests/test_lemmas.py).
+        const uint32_t hv0 = hx | (x & 1u);
+        const uint32_t q = x & ~t;
+        const uint32_t P0 = q & ~(q + (hv0 & ~t));
+        const uint32_t cin = carry_in_fwd(((x & ~P0) >> 31) != 0u, x == FULL) & x & 1u;
         const uint32_t lead = x & ~(x + 1);
-        const uint32_t S_ = s | (cin ? lead : 0u);
-        uint32_t ft = t & ~(((s << 1) & x & (x << 1)) | (cin ? lead : 0u));
+        const uint32_t P = cin ? (P0 & ~lead) : P0;
+        const uint32_t S_ = x & ~P;
+        uint32_t ft = t & ((P << 1) | (cin ? hx : hv0));
         uint32_t mc = upper_merge_heads(hu, u, up, x, xp, S_);
         // (K2 also drops the edges whose gap pixel is a hole bridged from the
         // row above -- redundant ones; here the merges are shared out over the
@@ -718,12 +737,14 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
                 // copied the same upper-strip run, so it is compressed too
                 const uint32_t j = vp[k];
                 uint32_t r = j;
-                // (j is never flagged: only this warp ranks its own runs, below)
-                while (true) {
-                    const uint32_t v = vp[r];
-                    if (v == r || (v & 0x8000u)) break;
-                    r = v;
-                }
+                // (j is never flagged: only this warp ranks its own runs,
+                // below; j == k: a root, no second load)
+                if (j != (uint32_t)k)
+                    while (true) {
+                        const uint32_t v = vp[r];
+                        if (v == r || (v & 0x8000u)) break;
+                        r = v;
+                    }
                 root = r == (uint32_t)k;
                 if (!root) {
                     vp[k] = (uint16_t)r;
@@ -756,42 +777,53 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
     const int64_t dstride = (int64_t)g.nTx * g.maxrun;
-    uint16_t *dst = ws.runcomp + ((int64_t)(R0 + r0) * g.nTx + tx) * g.maxrun - dstride;
+    {
+        // every run -> runcomp = (root row << 9) | rank of the root in its
+        // row; the component is rowfirst[row] + rank (K5 needs the row).  A
+        // per-lane loop (no ballot, no warp-uniform chunking): the row's only
+        // loop-carried state is o.
+        uint16_t *dst = ws.runcomp + ((int64_t)(R0 + r0) * g.nTx + tx) * g.maxrun;
+#pragma unroll 1
+        for (int i = 0; i < SR; i++, dst += dstride) {
+            const int rl = r0 + i, n = sm.nrun[rl];
+            const uint16_t *prow = sm.p + kidx(rl, 0);
+#pragma unroll 1
+            for (int o = lane; o < n; o += 32) {
+                const uint32_t pk = prow[o];
+                const uint32_t r = (pk & 0x8000u) ? (uint32_t)kidx(rl, o) : pk;
+                const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
+                dst[o] = (uint16_t)(((r / MR) << 9) | (pr & 0x1FFu));
+            }
+        }
+    }
+    // border roots (rows with any; most rows have none): nodes of the global
+    // union-find in index order, key = (image row, tile column, run ordinal)
 #pragma unroll 1
     for (int i = 0; i < SR; i++) {
-        const int rl = r0 + i, n = sm.nrun[rl];
-        dst += dstride;
+        const int rl = r0 + i;
+        if (sm.bcnt[rl] == 0) continue;  // warp-uniform
+        const int n = sm.nrun[rl];
         int bi = __shfl_sync(FULL, bfirst, rl);
         const int rf = __shfl_sync(FULL, rowfirst, rl);
-        const bool hasb = sm.bcnt[rl] != 0;
         const uint32_t *brow = bbits + rl * WPR;
 #pragma unroll 1
         for (int o0 = 0; o0 < n; o0 += 32) {
-            const int o = o0 + lane, k = kidx(rl, o);
-            const uint32_t pk = o < n ? sm.p[k] : 0u;
-            const int r = (pk & 0x8000u) ? k : (int)pk;
-            const uint32_t pr = (pk & 0x8000u) ? pk : sm.p[r];
-            if (o < n) {
-                // runcomp = (root row << 9) | rank of the root in its row; the
-                // component is rowfirst[row] + rank (K5 needs the row)
-                dst[o] = (uint16_t)(((uint32_t)(r / MR) << 9) | (pr & 0x1FFu));
+            const int o = o0 + lane;
+            const uint32_t pk = o < n ? sm.p[kidx(rl, o)] : 0u;
+            // node number of the chunk's first border root, for P4c
+            // (hbase is free after P2b)
+            if (lane == 0) sm.hbase[rl][o0 >> 5] = (uint16_t)bi;
+            const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
+            const uint32_t bbal = __ballot_sync(FULL, broot);
+            if (broot) {  // a root of this row: component rowfirst[row] + rank
+                const int c = rf + (int)(pk & 0x1FFu);
+                const int node = nodebase + bi + __popc(bbal & ((1u << lane) - 1u));
+                if (BANDS) compnode[c] = node;  // only the row-band path reads it
+                ws.gparent[node] = node;
+                ws.gnodecomp[node] = (rl << 16) | c;
+                ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
             }
-            if (hasb) {
-                // node number of the chunk's first border root, for P4c
-                // (hbase is free after P2b)
-                if (lane == 0) sm.hbase[rl][o0 >> 5] = (uint16_t)bi;
-                const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
-                const uint32_t bbal = __ballot_sync(FULL, broot);
-                if (broot) {  // a root of this row: component rowfirst[row] + rank
-                    const int c = rf + (int)(pk & 0x1FFu);
-                    const int node = nodebase + bi + __popc(bbal & ((1u << lane) - 1u));
-                    if (BANDS) compnode[c] = node;  // only the row-band path reads it
-                    ws.gparent[node] = node;
-                    ws.gnodecomp[node] = (rl << 16) | c;
-                    ws.gkey[node] = ((int64_t)(g.row0 + R0 + rl) * g.nTx + tx) * MAXRUN + o;
-                }
-                bi += __popc(bbal);
-            }
+            bi += __popc(bbal);
         }
     }
     __syncthreads();

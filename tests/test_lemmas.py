@@ -160,3 +160,57 @@ def test_threshold_bit_trick_all_byte_pairs():
         f = ((A & ~T4) | ((A | ~T4) & s)) & M
         got = (f >> (sh + np.uint64(7))) & np.uint64(1)
         assert np.array_equal(got.astype(bool), np.broadcast_to(a > t, got.shape))
+
+
+def _first_touch_words(xs, ts, B):
+    """K1 P2a's first-touch / smear by one addition per lane-word (see
+    ccl_kernels.cu P2a): returns (ft, S) per word."""
+    F = (1 << B) - 1
+    n = len(xs)
+    P0, hv0, hx = [], [], []
+    for l in range(n):
+        x, t = xs[l], ts[l]
+        xp = xs[l - 1] if l > 0 else 0
+        h = x & ~((x << 1) | (xp >> (B - 1))) & F
+        hv = (h | (x & 1)) & F
+        q = x & ~t & F
+        P0.append(q & ~((q + (hv & ~t & F)) & F) & F)
+        hv0.append(hv)
+        hx.append(h)
+    C = []
+    for l in range(n):
+        g = (xs[l] >> (B - 1)) & 1 == 1 and (P0[l] >> (B - 1)) & 1 == 0
+        C.append(g or (xs[l] == F and (C[l - 1] if l else False)))
+    out = []
+    for l in range(n):
+        x, t = xs[l], ts[l]
+        cin = (C[l - 1] if l else False) and (x & 1) == 1
+        lead = x & ~(x + 1) & F
+        P = (P0[l] & ~lead) if cin else P0[l]
+        out.append((t & (((P << 1) & F) | (hx[l] if cin else hv0[l])), x & ~P & F))
+    return out
+
+
+@pytest.mark.parametrize("B,lanes", [(4, 6), (8, 4), (32, 6)])
+def test_first_touch_by_addition(B, lanes):
+    """ft = the first touch pixel of every run of x, S = the run pixels at or
+    after it, across lane-words (carries through all-ones words), against a
+    direct left-to-right walk."""
+    rng = np.random.default_rng(B * 100 + lanes)
+    for _ in range(3000 if B < 32 else 400):
+        dens = rng.choice([0.5, 0.7, 0.95])
+        X = rng.random(B * lanes) < dens
+        T = X & (rng.random(B * lanes) < rng.choice([0.05, 0.3, 0.7]))
+        ft_ref, s_ref, seen = [], [], False
+        for i in range(B * lanes):
+            if not X[i]:
+                seen = False
+            ft_ref.append(bool(X[i] and T[i] and not seen))
+            seen = seen or bool(X[i] and T[i])
+            s_ref.append(bool(X[i] and seen))
+        xs = [int(sum(int(X[l * B + b]) << b for b in range(B))) for l in range(lanes)]
+        ts = [int(sum(int(T[l * B + b]) << b for b in range(B))) for l in range(lanes)]
+        for l, (ft, S) in enumerate(_first_touch_words(xs, ts, B)):
+            for b in range(B):
+                assert (ft >> b) & 1 == ft_ref[l * B + b]
+                assert (S >> b) & 1 == s_ref[l * B + b]
