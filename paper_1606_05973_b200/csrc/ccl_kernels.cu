@@ -378,8 +378,8 @@ struct K1SmemT {
     // the roots of components that touch the tile border (run k = r*MAXRUN+o
     // -> word [r][o/32], so every warp clears exactly the words it read)
     uint32_t mc[TH][WPR];
-    // P0b-P2b: runs whose head lies in earlier words of the row; P4 on:
-    // node number of the first border root of each 32-run chunk of the row
+    // P0b-P2b: runs whose head lies in earlier words of the row; P4 on: row
+    // w holds warp w's copy of the border nodes before each tile row
     uint16_t hbase[TH][WPR];
     int32_t nrun[TH];              // runs per row
     int32_t rowcnt[TH];            // components whose root run lies in the row
@@ -774,6 +774,13 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     const int rowfirst = (int)warp_excl_scan((uint32_t)sm.rowcnt[lane], rtot);  // lane = row
     const int bfirst = (int)warp_excl_scan((uint32_t)sm.bcnt[lane], btot);
     const int ncomp = (int)rtot, nborder = (int)btot;
+    // this warp's copy of the border nodes before each row (lane = row), for
+    // the node lookups below in lane-divergent code (hbase is free after P2b;
+    // every warp has its own row of it, so no barrier follows P3's)
+    static_assert(WPR == TH, "hbase rows hold one entry per tile row");
+    uint16_t *bfrow = sm.hbase[w];
+    bfrow[lane] = (uint16_t)bfirst;
+    __syncwarp();
     int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int nodebase = tile * g.capb;
     const int64_t dstride = (int64_t)g.nTx * g.maxrun;
@@ -810,9 +817,6 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
         for (int o0 = 0; o0 < n; o0 += 32) {
             const int o = o0 + lane;
             const uint32_t pk = o < n ? sm.p[kidx(rl, o)] : 0u;
-            // node number of the chunk's first border root, for P4c
-            // (hbase is free after P2b)
-            if (lane == 0) sm.hbase[rl][o0 >> 5] = (uint16_t)bi;
             const bool broot = o < n && (pk & 0x8000u) && ((brow[o >> 5] >> (o & 31)) & 1u);
             const uint32_t bbal = __ballot_sync(FULL, broot);
             if (broot) {  // a root of this row: component rowfirst[row] + rank
@@ -826,27 +830,35 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
             bi += __popc(bbal);
         }
     }
-    __syncthreads();
     K1_STOP(stop <= 4);
     // ---- P4c: nodes of the border pixels (for K2).  A border run's root r is
-    // a border root; its node is the chunk's first node number (P4) plus the
-    // border roots before it in its bitmap word -- all in shared memory.
+    // a border root; its node is the border roots of earlier rows (bfrow)
+    // plus those before it in its row's bitmap words -- all in shared memory,
+    // final since P3's barrier.  Top row, bottom row and the rows' end runs
+    // as one list over the CTA.
     {
         auto node_of = [&](int k) -> int {
             const uint32_t pk = sm.p[k];
             const int r = (pk & 0x8000u) ? k : (int)pk;
             const int rr = r / MR, ro = r % MR;
-            return nodebase + sm.hbase[rr][ro >> 5] + __popc(bbits[rr * WPR + (ro >> 5)] & ((1u << (ro & 31)) - 1u));
+            const uint32_t *bw = bbits + rr * WPR;
+            int nd = nodebase + bfrow[rr] + __popc(bw[ro >> 5] & ((1u << (ro & 31)) - 1u));
+            for (int j = 0; j < (ro >> 5); j++) nd += __popc(bw[j]);
+            return nd;
         };
         const int ntop = sm.nrun[0], nbot = sm.nrun[rows - 1];
-        for (int o = threadIdx.x; o < ntop; o += NWK * 32)
-            ws.topnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(0, o));
-        for (int o = threadIdx.x; o < nbot; o += NWK * 32)
-            ws.botnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(rows - 1, o));
-        for (int r = threadIdx.x; r < rows; r += NWK * 32) {
-            const int64_t off = (int64_t)tx * g.H + R0 + r;
-            ws.leftnode[off] = (sm.bm[r][0] & 1u) ? node_of(kidx(r, 0)) : -1;
-            ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? node_of(kidx(r, sm.nrun[r] - 1)) : -1;
+        for (int it = threadIdx.x; it < ntop + nbot + rows; it += NWK * 32) {
+            if (it < ntop) {
+                ws.topnode[(int64_t)tile * g.maxrun + it] = node_of(kidx(0, it));
+            } else if (it < ntop + nbot) {
+                const int o = it - ntop;
+                ws.botnode[(int64_t)tile * g.maxrun + o] = node_of(kidx(rows - 1, o));
+            } else {
+                const int r = it - ntop - nbot;
+                const int64_t off = (int64_t)tx * g.H + R0 + r;
+                ws.leftnode[off] = (sm.bm[r][0] & 1u) ? node_of(kidx(r, 0)) : -1;
+                ws.rightnode[off] = ((sm.bm[r][lc >> 5] >> (lc & 31)) & 1u) ? node_of(kidx(r, sm.nrun[r] - 1)) : -1;
+            }
         }
     }
     // the first and last row's run masks for K2's horizontal edges
