@@ -746,9 +746,9 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
                         r = v;
                     }
                 root = r == (uint32_t)k;
-                if (!root) {
+                if (j != r) {  // more than one hop (a root has j == r == k)
                     vp[k] = (uint16_t)r;
-                    if (j != r) vp[j] = (uint16_t)r;
+                    vp[j] = (uint16_t)r;
                 }
                 if (edge_row || (o == 0 && lfirst) || (o == n - 1 && llast)) {
                     const uint32_t bit = 1u << (r & 31);
