@@ -342,9 +342,8 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t *__restrict__ img, c
 // neighbours are in the tile, bridged by the pixel above or below inside the
 // tile).  *fg receives the foreground word itself.
 __device__ __forceinline__ uint32_t run_mask(const Geometry &g, const uint32_t *__restrict__ bm,
-                                             int row, int gword, uint32_t *fg) {
+                                             int row, int gword, int rl, int rows, uint32_t *fg) {
     const int lane = lane_id();
-    const int ty = row_tile(g, row), R0 = tile_r0(g, ty), rl = row - R0, rows = tile_rows(g, ty);
     const bool ok = gword < g.WW;
     const int64_t i = (int64_t)row * g.WW + gword;
     const uint32_t x0 = ok ? __ldcg(bm + i) : 0u;
@@ -1613,6 +1612,13 @@ static bool small_mode(const Geometry &g) {
 // j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
 // warp is one contiguous 512-byte stretch of the output row.
 constexpr int K5_WARPS = 16;  // measured vs 4 and 8
+// (x & bit) ? v : 0
+__device__ __forceinline__ int sel_bit(uint32_t x, uint32_t bit, int v) {
+    int r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %1, 0;\n\tselp.b32 %0, %2, 0, p;\n\t}"
+        : "=r"(r) : "r"(x & bit), "r"(v));
+    return r;
+}
 __global__ void __launch_bounds__(K5_WARPS * 32, 4)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, int mshift) {
     pdl_trigger();
@@ -1653,7 +1659,7 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
     const int nlv = lane < g.capc ? __ldcg(nrlab + lane) : 0;
     const int nlv2 = lane + 32 < g.capc ? __ldcg(nrlab + 32 + lane) : 0;
     uint32_t x;                                          // foreground
-    const uint32_t f = run_mask(g, ws.bm, row, gword, &x);  // runs
+    const uint32_t f = run_mask(g, ws.bm, row, gword, row - tile_r0(g, ty), tile_rows(g, ty), &x);  // runs
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
@@ -1706,34 +1712,45 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
     int32_t *out = labels + (int64_t)row * g.W + C0;
     uint64_t pol_first;  // labels are not read again: evict first (bm, runcomp stay in L2)
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-    const int b0 = 4 * (lane & 7);  // lane's 4 pixels inside lane-word 4c + lane/8
-    const uint32_t m0 = upto(b0);
-    // labels of pixels 128c + 4*lane .. +3.  Heads of the run mask are never
-    // adjacent, so pixels b0+1..b0+3 lie in the run of pixel b0 or one of the
-    // next two: three independent shared loads and selects
-    auto quad = [&](int c, int &v0, int &v1, int &v2, int &v3) {
-        const uint4 t = s_word[wi][4 * c + (lane >> 3)];
-        const uint32_t nib = t.x >> b0, hn = t.y >> b0;
-        const int32_t *rp = rowlab + ((int)t.z + __popc(t.y & m0) - 1);  // run containing (or before) pixel b0
+    // labels of 4 pixels b..b+3 of lane-word t.  Heads of the run mask are
+    // never adjacent, so pixels b+1..b+3 lie in the run of pixel b or one of
+    // the next two: three independent shared loads and selects
+    auto quad_at = [&](const uint4 &t, int b, uint32_t mb, int &v0, int &v1, int &v2, int &v3) {
+        const uint32_t nib = t.x >> b, hn = t.y >> b;
+        const int32_t *rp = rowlab + ((int)t.z + __popc(t.y & mb) - 1);  // run containing (or before) pixel b
         const int l0 = rp[0], l1 = rp[1], l2 = rp[2];
         const int a1 = (hn & 2u) ? l1 : l0;
         const int a2 = (hn & 6u) ? l1 : l0;
         const int a3 = (hn & 8u) ? ((hn & 2u) ? l2 : l1) : a2;
-        v0 = (nib & 1u) ? l0 : 0;
-        v1 = (nib & 2u) ? a1 : 0;
-        v2 = (nib & 4u) ? a2 : 0;
-        v3 = (nib & 8u) ? a3 : 0;
+        // (a predicate test + select per pixel: two instructions; the plain
+        // `? l : 0` compiles to a three-instruction sign mask)
+        v0 = sel_bit(nib, 1u, l0);
+        v1 = sel_bit(nib, 2u, a1);
+        v2 = sel_bit(nib, 4u, a2);
+        v3 = sel_bit(nib, 8u, a3);
     };
-    if (g.aligned && vcols == TW) {  // interior segment: eight full 512-byte warp stores
+    if (g.aligned && vcols == TW && ((reinterpret_cast<uintptr_t>(out) & 31u) == 0)) {
+        // interior segment: four full 1024-byte warp stores (256-bit per
+        // lane: pixels 256c + 8*lane .. +7, two quads of lane-word 8c + lane/4)
+        const int b8 = 8 * (lane & 3);
+        const uint32_t mA = upto(b8), mB = upto(b8 + 4);
 #pragma unroll
-        for (int c = 0; c < 8; c++) {
-            int v0, v1, v2, v3;
-            quad(c, v0, v1, v2, v3);
-            asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out + 128 * c + 4 * lane),
-                         "r"(v0), "r"(v1), "r"(v2), "r"(v3), "l"(pol_first) : "memory");
+        for (int c = 0; c < 4; c++) {
+            const uint4 t = s_word[wi][8 * c + (lane >> 2)];
+            int v0, v1, v2, v3, v4, v5, v6, v7;
+            quad_at(t, b8, mA, v0, v1, v2, v3);
+            quad_at(t, b8 + 4, mB, v4, v5, v6, v7);
+            asm volatile("st.global.L2::cache_hint.v8.s32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;"
+                         ::"l"(out + 256 * c + 8 * lane), "r"(v0), "r"(v1), "r"(v2), "r"(v3),
+                         "r"(v4), "r"(v5), "r"(v6), "r"(v7), "l"(pol_first) : "memory");
         }
         return;
     }
+    const int b0 = 4 * (lane & 7);  // lane's 4 pixels inside lane-word 4c + lane/8
+    const uint32_t m0 = upto(b0);
+    auto quad = [&](int c, int &v0, int &v1, int &v2, int &v3) {
+        quad_at(s_word[wi][4 * c + (lane >> 3)], b0, m0, v0, v1, v2, v3);
+    };
 #pragma unroll 1
     for (int c = 0; c < 8; c++) {
         const int P = 128 * c + 4 * lane;
@@ -1767,10 +1784,11 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
     const int row = side ? g.H - 1 : 0;
     keys += side * g.W;
     nodes += side * g.W;
-    const int C0 = tx * TW, tile = row_tile(g, row) * g.nTx + tx;
+    const int ty = row_tile(g, row);
+    const int C0 = tx * TW, tile = ty * g.nTx + tx;
     const int gword = tx * WPR + lane;
     uint32_t x;
-    const uint32_t f = run_mask(g, ws.bm, row, gword, &x);
+    const uint32_t f = run_mask(g, ws.bm, row, gword, row - tile_r0(g, ty), tile_rows(g, ty), &x);
     const uint32_t fl = __shfl_up_sync(FULL, f, 1);
     const uint32_t hx = f & ~((f << 1) | (lane == 0 ? 0u : (fl >> 31)));
     uint32_t nr;
