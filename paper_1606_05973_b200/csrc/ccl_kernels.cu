@@ -498,6 +498,17 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     if (g.aligned && C0 + TW <= g.W && rows == TH) {  // interior tile: all 2*SR loads in flight
         const uint8_t *src = img + (int64_t)(R0 + r0) * g.W + C0 + 32 * lane;
         uint4 v[2 * SR];
+        if (((reinterpret_cast<uintptr_t>(img) | (uintptr_t)g.W) & 31u) == 0) {
+            // rows 32-byte aligned: one 256-bit load per lane and row (K1
+            // 279 -> 273 us on C4 against two 128-bit loads)
+#pragma unroll
+            for (int i = 0; i < SR; i++) {
+                uint4 &a = v[2 * i], &b = v[2 * i + 1];
+                asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                             : "l"(src + (int64_t)i * g.W));
+            }
+        } else
 #pragma unroll
         for (int i = 0; i < SR; i++) {
             v[2 * i] = __ldcs(reinterpret_cast<const uint4 *>(src + (int64_t)i * g.W));
