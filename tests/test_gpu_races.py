@@ -120,13 +120,16 @@ def test_small_path_chains_repeated():
 
 def test_unaligned_base_pointers():
     """W % 16 == 0 but img / labels base pointers off 16-byte alignment: the
-    kernels must take the narrow paths (no misaligned vector access)."""
+    kernels must take the narrow paths (no misaligned vector access); and
+    16-byte but not 32-byte aligned bases (the 128-bit paths instead of
+    K1's 256-bit loads and K5's 256-bit stores)."""
     H, W = 200, 2048
     img = synth.bernoulli(H, W, 0.45, seed=9)
     lo, no = oracle.label(img)
-    for ioff, loff in ((1, 0), (0, 1), (3, 2), (8, 3)):
-        ib = torch.zeros(H * W + 16, dtype=torch.uint8, device="cuda")
+    for ioff, loff in ((1, 0), (0, 1), (3, 2), (8, 3), (16, 4), (16, 0), (0, 4)):
+        ib = torch.zeros(H * W + 64, dtype=torch.uint8, device="cuda")
         lb = torch.zeros(H * W + 16, dtype=torch.int32, device="cuda")
+        assert ib.data_ptr() % 32 == 0 and lb.data_ptr() % 32 == 0
         it = ib[ioff:ioff + H * W].view(H, W)
         it.copy_(torch.from_numpy(img))
         out = lb[loff:loff + H * W].view(H, W)
