@@ -141,6 +141,7 @@ using namespace cclb;
 
 struct ccl_plan_st {
     Geometry g;
+    int32_t *hint = nullptr;  // mapped pinned host word: K1's last hand-over count
     void *ws_mem = nullptr;
     size_t ws_bytes = 0;
     Workspace ws;
@@ -272,9 +273,23 @@ ccl_status ccl_plan_create_batch(int B, int H, int W, ccl_plan *plan_out) {
         return e == cudaErrorMemoryAllocation ? CCL_OUT_OF_MEMORY : CCL_CUDA_ERROR;
     }
     p->ws = workspace_bind(p->g, p->ws_mem);
+    // the hand-over hint word (see Workspace::k1hint_dev)
+    int32_t *hint = nullptr, *hint_dev = nullptr;
+    if (cudaHostAlloc(&hint, sizeof(int32_t), cudaHostAllocMapped) == cudaSuccess) {
+        *hint = -1;
+        if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&hint_dev), hint, 0) == cudaSuccess) {
+            p->hint = hint;
+            p->ws.k1hint_dev = hint_dev;
+            p->ws.k1hint_host = hint;
+        } else {
+            cudaFreeHost(hint);
+        }
+    }
+    cudaGetLastError();  // (no hint: the full hand-over grid every call)
     if (workspace_poison(p->ws_mem, p->ws_bytes, 0) != cudaSuccess || workspace_init(p->ws, 0) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {
         cudaFree(p->ws_mem);
+        if (p->hint) cudaFreeHost(p->hint);
         delete p;
         return CCL_CUDA_ERROR;
     }
@@ -327,6 +342,7 @@ ccl_status ccl_plan_destroy(ccl_plan p) {
     free_host_pipe(p);
     cudaError_t e = cudaSuccess;
     if (p->ws_mem) e = cudaFree(p->ws_mem);
+    if (p->hint) cudaFreeHost(p->hint);
     free_events(p);
     delete p;
     return e == cudaSuccess ? CCL_OK : CCL_CUDA_ERROR;

@@ -72,6 +72,12 @@ struct Workspace {
     int32_t *k1over;      // [nT]              tiles K1 handed to its full-size pass
     int32_t *k1over_n;    // [1]               their count (0 between calls; K3 resets it)
     unsigned long long *stats;  // [STAT_COUNT]  cumulative path counters (ccl_plan_counters)
+    // plans only (null otherwise): K3 stores the number of tiles K1 handed
+    // over into a mapped pinned host word; the host sizes the next call's
+    // hand-over pass from the last value it sees (a grid of 370 idle CTAs
+    // held K2's launch back by ~10 us on C4; the comb needs the full grid)
+    int32_t *k1hint_dev = nullptr;                  // device address of the word
+    const volatile int32_t *k1hint_host = nullptr;  // host address (-1: nothing seen yet)
     // row bands only (null for a whole image):
     const int32_t *xlab;  // [nb*2W]           exported labels of all bands' boundary slots; a
                           //                   node whose parent is -2-f takes xlab[f]

@@ -1145,7 +1145,10 @@ __global__ void __launch_bounds__(NWN * 32, NWN == 8 ? 6 : 16)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
     pdl_trigger();
     pdl_wait();
-    if (blockIdx.x == 0 && threadIdx.x == 0) *ws.k1over_n = 0;  // K1's hand-over list, for the next call
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (ws.k1hint_dev) *reinterpret_cast<volatile int32_t *>(ws.k1hint_dev) = __ldcg(ws.k1over_n);
+        *ws.k1over_n = 0;  // K1's hand-over list, for the next call
+    }
     __shared__ KNSmem<NWN> sm;
     const int lane = lane_id(), w = threadIdx.x >> 5;
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
@@ -2034,8 +2037,12 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
         auto k1b = g.thr ? (batch ? k_tile_big<true, true> : bands ? k_tile_big<true, false, true> : k_tile_big<true, false>)
                          : (batch ? k_tile_big<false, true> : bands ? k_tile_big<false, false, true> : k_tile_big<false, false>);
         // a small grid (usually there is nothing to do; its CTAs loop over the list)
-        e = launch_pdl(k1b, std::min(g.nT, g_k1big_resident / 2), NW * 32, sizeof(K1Smem), stream, img, g, ws,
-                       g_k1_stop);
+        // (a plan's last known hand-over count of 0: a quarter of the SMs, so
+        // that every CTA fits beside K1's last wave and K2 is scheduled at
+        // once -- C4 step 661 -> 650 us; otherwise half the resident slots)
+        const bool idle = ws.k1hint_host && *ws.k1hint_host == 0;
+        const int grid = idle ? std::max(1, g_sms / 4) : g_k1big_resident / 2;
+        e = launch_pdl(k1b, std::min(g.nT, grid), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
         if (e != cudaSuccess) return e;
     }
     mark(K_BORDER);

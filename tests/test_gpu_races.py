@@ -196,3 +196,28 @@ def test_plans_on_concurrent_streams(name, h, w):
         lo, no = want[j]
         assert int(n.item()) == no
         assert np.array_equal(out.cpu().numpy(), lo), j
+
+
+@pytest.mark.gpu
+def test_handover_grid_adapts_per_plan():
+    """A plan sizes K1's hand-over pass from the last hand-over count it saw
+    (a mapped host word written by K3): after calls with no handed-over
+    tiles the pass is launched small; an image that then hands over every
+    tile must still be labelled in full, and the plan must grow back."""
+    H, W = 2048, 4096
+    quiet = synth.bernoulli(H, W, 0.15, seed=21)
+    dense = _handed_over_dense(H, W, seed=23)
+    want = {k: oracle.label(im) for k, im in (("q", quiet), ("d", dense))}
+    plan = ccl.Plan(H, W)
+    out = torch.empty((H, W), dtype=torch.int32, device="cuda")
+    n = torch.empty(1, dtype=torch.int32, device="cuda")
+    seq = ["q"] * 4 + ["d"] * 3 + ["q"] * 3 + ["d", "q", "d"]
+    gpu = {k: torch.from_numpy(im).cuda() for k, im in (("q", quiet), ("d", dense))}
+    for i, k in enumerate(seq):
+        before = plan.counters()["k1_handover"]
+        plan.label(gpu[k], out, n)
+        torch.cuda.synchronize()
+        after = plan.counters()["k1_handover"]
+        assert int(n.item()) == want[k][1], (i, k)
+        assert np.array_equal(out.cpu().numpy(), want[k][0]), (i, k)
+        assert (after > before) == (k == "d"), (i, k, before, after)
