@@ -886,11 +886,15 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
     }
 }
 
+#ifndef K1_SR
+#define K1_SR S  // rows per warp of the main K1 (TH / K1_SR warps per CTA)
+#endif
+constexpr int K1_THREADS = TH / K1_SR * 32;
 template <bool THR, bool BATCH, bool BANDS = false>
 #ifndef K1_MINB
 #define K1_MINB 6  // CTAs per SM (40 registers; 7 forces 32 and spills)
 #endif
-__global__ void __launch_bounds__(NW * 32, K1_MINB)
+__global__ void __launch_bounds__(K1_THREADS, K1_MINB)
 k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd, int pfx, int pfy, int stop) {
     pdl_trigger();
     // a 2-D grid (tile columns x tile rows; CTAs still start in raster
@@ -905,7 +909,7 @@ k_tile_local(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int pfd,
         tx = tile % g.nTx;
         ty = tile / g.nTx;
     }
-    k1_tile<THR, BATCH, BANDS, K1_MR>(img, g, ws, tile, tx, ty, pfd, pfx, pfy, stop);
+    k1_tile<THR, BATCH, BANDS, K1_MR, K1_SR>(img, g, ws, tile, tx, ty, pfd, pfx, pfy, stop);
 }
 
 // Images of few tiles (fewer than the SMs can hold twice over): one warp per
@@ -1983,7 +1987,7 @@ static cudaError_t set_attrs() {
     int dev = 0, sms = 0, per = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false, false>, NW * 32,
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_local<false, false>, K1_THREADS,
                                                            sizeof(K1SmemT<K1_MR>))) != cudaSuccess)
         return e;
     g_k1_resident = sms * per;
@@ -2029,7 +2033,7 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
                         : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
         const int pfd = g_k1_exper ? 0 : g_k1_resident / 4;
         const bool twod = g.nTy <= 65535;
-        e = launch_pdl2(k1, twod ? dim3(g.nTx, g.nTy) : dim3(g.nT), NW * 32, sizeof(K1SmemT<K1_MR>), stream, img, g,
+        e = launch_pdl2(k1, twod ? dim3(g.nTx, g.nTy) : dim3(g.nT), K1_THREADS, sizeof(K1SmemT<K1_MR>), stream, img, g,
                         ws, pfd, pfd % g.nTx, pfd / g.nTx, g_k1_stop);
     }
     if (e != cudaSuccess) return e;
