@@ -1134,6 +1134,21 @@ k_fixup(Geometry g, Workspace ws) {
 //                  nonroots_before(c);
 //   gnodelab       the labels of the tile's root border nodes (K4 reads them
 //                  for the components merged into them).
+#if CCL_K3_TRACE
+// development trace (build knob; scripts/k3_trace.py): per tile row,
+// globaltimer at the kernel's entry, after pdl_wait, after phase 1, after
+// phase 2, after the lookback barrier and at the end
+__device__ unsigned long long g_k3trace[4096][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define K3T(ty, i) \
+    if (threadIdx.x == 0 && (ty) < 4096) g_k3trace[ty][i] = gtimer()
+#else
+#define K3T(ty, i) (void)0
+#endif
 template <int NWN>
 struct KNSmem {
     int32_t nrrow[NWN][TH];           // non-root border components per row
@@ -1147,6 +1162,9 @@ struct KNSmem {
 template <int NWN>
 __global__ void __launch_bounds__(NWN * 32, NWN == 8 ? 6 : 16)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
+#if CCL_K3_TRACE
+    const unsigned long long t_in = gtimer();
+#endif
     pdl_trigger();
     pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1158,6 +1176,10 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     if (threadIdx.x == 0) sm.part = atomicAdd(ws.ticket, 1);
     __syncthreads();
     const int ty = sm.part;
+#if CCL_K3_TRACE
+    if (threadIdx.x == 0 && ty < 4096) g_k3trace[ty][0] = t_in;
+#endif
+    K3T(ty, 1);
     const int R0 = tile_r0(g, ty), rows = tile_rows(g, ty);
     const bool first = ty % g.tpi == 0;  // first tile row of its image: numbering starts at 1
     // ---- phase 1: non-root border components of every tile (bitmap, prefix,
@@ -1223,6 +1245,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         __syncwarp();
     }
     __syncthreads();
+    K3T(ty, 2);
     // ---- phase 2: exclusive scan of the tile row's rows*nTx segment counts
     // (raster order), then the lookback over earlier tile rows
     const int64_t sbase = (int64_t)R0 * g.nTx;
@@ -1255,6 +1278,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         carry += all;
         __syncthreads();  // wsum reuse
     }
+    K3T(ty, 3);
     // descriptor: bits 62-63 status (1 aggregate, 2 inclusive prefix), low 32
     // bits value.  Warp 0 looks back over 32 predecessors at a time.
     if (w == 0) {
@@ -1271,7 +1295,12 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
                 const uint32_t incl = __ballot_sync(FULL, s2 == 2), zero = __ballot_sync(FULL, s2 == 0);
                 const int first = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive prefix
                 const uint32_t need = (2u << first) - 1u;         // lanes 0..first
-                if (zero & need) continue;                        // not all published yet: spin
+                if (zero & need) {                                // not all published yet: spin
+#if CCL_K3_BACKOFF
+                    __nanosleep(CCL_K3_BACKOFF);
+#endif
+                    continue;
+                }
                 int v = lane <= first ? (int)(uint32_t)d : 0;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -1292,6 +1321,7 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
     __syncthreads();
     // ---- phase 3: label bases of every tile row segment and the labels of
     // the root border nodes (offset(segment) + rank in segment + 1)
+    K3T(ty, 4);
     const int excl = sm.excl;
     for (int tx = w; tx < g.nTx; tx += NWN) {
         const int tile = ty * g.nTx + tx;
@@ -1321,7 +1351,16 @@ k_number(Geometry g, Workspace ws, int32_t *n_components) {
         }
     }
     if (threadIdx.x == 0) ws.rowexcl[ty] = excl;
+#if CCL_K3_TRACE
+    __syncthreads();
+    K3T(ty, 5);
+#endif
 }
+#if CCL_K3_TRACE
+extern "C" int ccl_debug_k3trace(unsigned long long *host, int rows) {
+    return (int)cudaMemcpyFromSymbol(host, g_k3trace, (size_t)rows * 6 * sizeof(unsigned long long));
+}
+#endif
 
 // ============================================================ small images
 // K2 + K3 + K4 in ONE CTA for images of one tile column and at most 32 tile
