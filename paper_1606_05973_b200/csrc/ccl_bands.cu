@@ -198,8 +198,8 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
     const int W = b.g.W;
     CK(run_stage_local(b.g, b.ws, img, s, ev));
     if (ev) CK(cudaEventRecord(ev[2], s));
-    CK(band_row_roots(b.g, b.ws, keys, b.d_nodes, s));
-    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, ++b.epoch, reps, spar, spar_lo, spar_hi, s));
+    CK(band_row_roots(b.g, b.ws, keys, b.d_nodes, b.d_noderep, ++b.epoch, s));
+    CK(band_rep(b.d_nodes, 2 * W, b.d_noderep, reps, spar, spar_lo, spar_hi, s));
     return CCL_OK;
 }
 

@@ -142,16 +142,18 @@ cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_c
 cudaError_t run_stage_final(const Geometry &g, const Workspace &ws, int32_t *labels,
                             cudaStream_t stream, cudaEvent_t *ev);
 // Row bands: per-pixel root key / root node of the band's first row (keys[0,W),
-// nodes[0,W)) and last row ([W,2W)); -1 for background.
+// nodes[0,W)) and last row ([W,2W)); -1 for background.  Also the
+// representative slot of every band-local root node: atomicMin of
+// ((~epoch) << 32 | slot) into noderep[node] over the run heads.
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys, int32_t *nodes,
-                           cudaStream_t stream);
+                           unsigned long long *noderep, uint32_t epoch, cudaStream_t stream);
 // Cross-band step (row bands).  Slots: band k's first
 // row then last row, W each, at k*2W.
-// rep[s] = first slot (of this band's 2W) with the same band-local root node;
-// noderep: one entry per node of the band, all-ones initially; epoch: a
-// number that grows with every call on the same scratch (starting at 1).
+// rep[s] = first slot (of this band's 2W) with the same band-local root node,
+// read from noderep (one entry per node of the band, all-ones initially;
+// epoch: a number that grows with every call on the same scratch, from 1).
 // Also starts the slot union-find: spar[t] = t for t in [spar_lo, spar_hi).
-cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
+cudaError_t band_rep(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep,
                      int32_t *spar, int spar_lo, int spar_hi, cudaStream_t stream);
 // The unions over all nb*2W slots (keys / reps of every band gathered).
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,

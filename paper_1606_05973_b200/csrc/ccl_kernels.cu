@@ -1829,7 +1829,7 @@ k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, 
 // Per pixel of a local row: the key and node of its component's root in the
 // band's forest (after k_border).  One warp per 1024-px row segment.
 __global__ void __launch_bounds__(256)
-k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
+k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes, unsigned long long *noderep, uint32_t epoch) {
     pdl_trigger();
     pdl_wait();
     __shared__ int32_t s_node[4][MAXRUN];
@@ -1870,6 +1870,11 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
         const int ord = (int)bw + __popc(hw & upto(lane)) - 1;
         keys[col] = fg ? s_key[wi][ord] : -1;
         nodes[col] = fg ? s_node[wi][ord] : -1;
+        // the representative slot of every band-local root node (its first
+        // slot: the minimum over the heads of its runs), see k_xb_rep2
+        if (fg && ((hw >> lane) & 1u))
+            atomicMin(noderep + s_node[wi][ord],
+                      ((unsigned long long)(0xFFFFFFFFu - epoch) << 32) | (uint32_t)(side * g.W + col));
     }
 }
 
@@ -1883,17 +1888,10 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes) {
 // in raster order (PARemSP's boundary merge).
 
 // Representative slot of every boundary slot of this band: the first slot
-// whose pixel has the same band-local root node.
-// noderep entries carry the call's epoch in their high word (stored
-// complemented, so a newer call's entries are smaller and win atomicMin):
-// the scratch never needs clearing.
-__global__ void k_xb_rep1(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch) {
-    pdl_trigger();
-    pdl_wait();
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < n && nodes[s] >= 0)
-        atomicMin(noderep + nodes[s], ((unsigned long long)(0xFFFFFFFFu - epoch) << 32) | (uint32_t)s);
-}
+// whose pixel has the same band-local root node (k_band_rows takes the
+// atomicMin over the run heads).  noderep entries carry the call's epoch in
+// their high word (stored complemented, so a newer call's entries are
+// smaller and win atomicMin): the scratch never needs clearing.
 // (also starts the slot union-find: every slot in [lo, hi) its own root)
 __global__ void k_xb_rep2(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep,
                           int32_t *spar, int lo, int hi) {
@@ -2192,17 +2190,15 @@ cudaError_t run_pipeline(const Geometry &g, const Workspace &ws, const uint8_t *
 }
 
 cudaError_t band_row_roots(const Geometry &g, const Workspace &ws, int64_t *keys, int32_t *nodes,
-                           cudaStream_t stream) {
-    return launch_pdl(k_band_rows, (2 * g.nTx + 3) / 4, 128, 0, stream, g, ws, keys, nodes);
+                           unsigned long long *noderep, uint32_t epoch, cudaStream_t stream) {
+    return launch_pdl(k_band_rows, (2 * g.nTx + 3) / 4, 128, 0, stream, g, ws, keys, nodes, noderep, epoch);
 }
 
-cudaError_t band_rep(const int32_t *nodes, int n, unsigned long long *noderep, uint32_t epoch, int32_t *rep,
+cudaError_t band_rep(const int32_t *nodes, int n, const unsigned long long *noderep, int32_t *rep,
                      int32_t *spar, int spar_lo, int spar_hi, cudaStream_t stream) {
-    cudaError_t e = launch_pdl(k_xb_rep1, (n + 255) / 256, 256, 0, stream, nodes, n, noderep, epoch);
-    if (e != cudaSuccess) return e;
     const int m = std::max(n, spar_hi - spar_lo);
-    return launch_pdl(k_xb_rep2, (m + 255) / 256, 256, 0, stream, nodes, n, (const unsigned long long *)noderep,
-                      rep, spar, spar_lo, spar_hi);
+    return launch_pdl(k_xb_rep2, (m + 255) / 256, 256, 0, stream, nodes, n, noderep, rep, spar, spar_lo,
+                      spar_hi);
 }
 
 cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps, int32_t *spar,
