@@ -411,9 +411,9 @@ def main():
         splan = ccl.ShardPlan(bh, W, row0, H, comm)
         step = lambda: splan.label(d_img, out, n_out)  # noqa: E731
         plan = None
-        # our kernels per band step (ccl_bands.cu): K1 (+ its hand-over pass), K2, boundary rows,
-        # 2 slot representatives (the second also starts the slot union-find),
-        # slot unions, link, K3, export (+ band offset), K4, K5 (the 3 NCCL
+        # our kernels per band step (ccl_bands.cu): K1 (+ its hand-over pass), K2, boundary rows
+        # (+ representative minima), slot representatives (+ the slot union-find's start),
+        # slot unions, link, K3, export, band offset, K4, K5 (the 2 NCCL
         # all-gathers are not counted)
         launches_per_step = 12
 

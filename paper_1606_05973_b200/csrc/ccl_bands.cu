@@ -4,12 +4,12 @@
 // label base, "count <- start x col"); the boundary rows of
 // all bands are all-gathered and every rank resolves the small cross-band
 // equivalence graph on its GPU (PARemSP's boundary merge);
-// per-band root counts are all-gathered so each band numbers its labels after
-// the earlier bands.  Everything stays on the device and on the stream: no
+// per-band root counts are all-gathered (with the band-local labels of the
+// boundary roots) so each band numbers its labels after the earlier bands.  Everything stays on the device and on the stream: no
 // host synchronization inside a call.
 //
 // Protocol per band (the same code drives NCCL ranks and the single-GPU
-// "virtual bands" mode, which only differs in how the three all-gathers move
+// "virtual bands" mode, which only differs in how the two all-gathers move
 // bytes):
 //   A  tile labeling + tile-edge merge of the band; per pixel of its first and
 //      last row the band-local root key and node (2W "slots"), and for every
@@ -19,10 +19,13 @@
 //      8-adjacency across every band boundary; the smaller key wins), then
 //      this band's components whose class starts elsewhere are linked: to the
 //      other component's node in this band, or to a foreign slot (-2-slot)
-//   C  roots + numbering scan of the band -> N_band
-//   X2 all-gather of N_band -> offset of this band = sum over earlier bands
-//   D  labels of the band's boundary-slot roots
-//   X3 all-gather of those labels = the foreign-label table (slot indexed)
+//   C  roots + numbering scan of the band -> N_band; the band-local labels
+//      of the band's boundary-slot roots (both need only the band itself)
+//   X2 all-gather of the band records (N_band, then those 2W labels): the
+//      foreign-label table and the counts in one collective (a foreign
+//      root's label = its band-local label + the N of the bands before its
+//      band; round 1 gathered N and the labels in two)
+//   D  offset of this band = sum of N over earlier bands; N
 //   E  labels of merged components + label write
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -123,20 +126,17 @@ struct XBand {
     int64_t *keys = nullptr;  // nb*2W slot keys (-1 background)
     int32_t *reps = nullptr;  // nb*2W representative slot (band-local index)
     int32_t *spar = nullptr;  // nb*2W slot union-find
-    int32_t *exps = nullptr;  // nb*2W exported labels
-    int32_t *counts = nullptr;  // nb   N of every band
+    int32_t *recs = nullptr;  // nb*(2W+1) band records: N_band, then its slots' band-local root labels
     ~XBand() { release(); }
     void release() {
         if (keys) cudaFree(keys);
         if (reps) cudaFree(reps);
         if (spar) cudaFree(spar);
-        if (exps) cudaFree(exps);
-        if (counts) cudaFree(counts);
+        if (recs) cudaFree(recs);
         keys = nullptr;
         reps = nullptr;
         spar = nullptr;
-        exps = nullptr;
-        counts = nullptr;
+        recs = nullptr;
     }
 };
 
@@ -179,16 +179,15 @@ ccl_status xband_init(XBand &x, int nb, int W) {
     CK(cudaMalloc(&x.keys, sizeof(int64_t) * n));
     CK(cudaMalloc(&x.reps, sizeof(int32_t) * n));
     CK(cudaMalloc(&x.spar, sizeof(int32_t) * n));
-    CK(cudaMalloc(&x.exps, sizeof(int32_t) * n));
-    CK(cudaMalloc(&x.counts, sizeof(int32_t) * nb));
+    CK(cudaMalloc(&x.recs, sizeof(int32_t) * ((size_t)nb * (2 * W + 1))));
     return CCL_OK;
 }
 
 // A: local labeling; slot keys / nodes / representatives into (keys, reps)
 // Profiling events of a band step (ShardPlan profiling), SHARD_EV per set:
 // 0 K1, 1 K2, 2 cross-band exchange (row roots, representatives,
-// all-gather, slot unions, links), 3 K3, 4 count all-gather + export +
-// label all-gather, 5 K4, 6 K5, 7 end.
+// all-gather, slot unions, links), 3 K3, 4 export + record all-gather +
+// offsets, 5 K4, 6 K5, 7 end.
 constexpr int SHARD_EV = 8;
 const char *const kShardNames[SHARD_EV - 1] = {"k_tile_local", "k_border", "xband_exchange", "k_number",
                                                 "xband_export", "k_fixup", "k_write"};
@@ -204,24 +203,27 @@ ccl_status band_phase_a(Band &b, const uint8_t *img, int64_t *keys, int32_t *rep
 }
 
 // B (after the slot tables are complete): link this band's components whose
-// class starts elsewhere.  C: roots + numbering scan -> N_band in counts[self].
-ccl_status band_phase_bc(Band &b, const XBand &x, int self, int32_t *count_out, cudaStream_t s,
-                         cudaEvent_t *ev = nullptr) {
+// class starts elsewhere.  C: roots + numbering scan -> N_band, then the
+// band-local labels of its slots' roots: the band's record (N_band, 2W
+// labels) of the gathered table, complete before the one all-gather X2.
+ccl_status band_phase_bc(Band &b, const XBand &x, int self, cudaStream_t s, cudaEvent_t *ev = nullptr) {
+    int32_t *rec = x.recs + (size_t)self * (2 * x.W + 1);
     CK(band_link(b.ws, x.W, self, x.keys, x.spar, b.d_nodes, s));
-    CK(run_stage_count(b.g, b.ws, count_out, s, ev ? ev + 3 : nullptr));  // ev[3]
+    CK(run_stage_count(b.g, b.ws, rec, s, ev ? ev + 3 : nullptr));  // ev[3]
+    if (ev) CK(cudaEventRecord(ev[4], s));
+    CK(band_export(b.g, b.ws, b.d_nodes, rec + 1, 2 * x.W, s));
     return CCL_OK;
 }
 
-// D: with all counts known, the band offset and the labels of its slots' roots
-ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, int32_t *exp_out,
-                        cudaStream_t s) {
-    CK(band_export(b.g, b.ws, b.d_nodes, exp_out, 2 * x.W, x.nb, self, x.counts, b.d_small + 1, n_total, s));
+// D (every record gathered): the band offset (N of earlier bands) and N
+ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, cudaStream_t s) {
+    CK(band_offsets(x.recs, x.nb, x.W, self, b.d_small + 1, n_total, s));
     return CCL_OK;
 }
 
-// E: labels of merged components (foreign ones from the exported table) + write
+// E: labels of merged components (foreign ones from the gathered records) + write
 ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s, cudaEvent_t *ev = nullptr) {
-    b.ws.xlab = x.exps;
+    b.ws.xlab = x.recs;
     CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 5 : nullptr));  // ev[5], ev[6], ev[7]
     return CCL_OK;
 }
@@ -267,13 +269,12 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
                                (int)(k * slots), (int)((k + 1) * slots), s)) != CCL_OK)
             return st;
     CK(band_resolve(nbands, W, x.keys, x.reps, x.spar, s));
-    // B + C (+ X2)
+    // B + C (+ X2: every band writes its record straight into the shared table)
     for (int k = 0; k < nbands; k++)
-        if ((st = band_phase_bc(bands[k], x, k, x.counts + k, s)) != CCL_OK) return st;
-    // D (+ X3)
+        if ((st = band_phase_bc(bands[k], x, k, s)) != CCL_OK) return st;
+    // D
     for (int k = 0; k < nbands; k++)
-        if ((st = band_phase_d(bands[k], x, k, k == 0 ? n_components : nullptr, x.exps + k * slots, s)) != CCL_OK)
-            return st;
+        if ((st = band_phase_d(bands[k], x, k, k == 0 ? n_components : nullptr, s)) != CCL_OK) return st;
     // E
     for (int k = 0; k < nbands; k++)
         if ((st = band_phase_e(bands[k], x, labels + (size_t)r0[k] * W, s)) != CCL_OK) return st;
@@ -397,12 +398,12 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     CKN(ncclGroupEnd());
     // B + C + X2
     CK(band_resolve(p->nranks, p->W, x.keys, x.reps, x.spar, s));
-    if ((st = band_phase_bc(b, x, self, x.counts + self, s, ev)) != CCL_OK) return st;
-    if (ev) CK(cudaEventRecord(ev[4], s));
-    CKN(ncclAllGather(x.counts + self, x.counts, 1, ncclInt32, p->comm, s));
-    // D + X3
-    if ((st = band_phase_d(b, x, self, n_components, x.exps + self * slots, s)) != CCL_OK) return st;
-    CKN(ncclAllGather(x.exps + self * slots, x.exps, slots, ncclInt32, p->comm, s));
+    if ((st = band_phase_bc(b, x, self, s, ev)) != CCL_OK) return st;
+    // X2: every band's record (N_band + its slots' band-local root labels)
+    const size_t rec = slots + 1;
+    CKN(ncclAllGather(x.recs + self * rec, x.recs, rec, ncclInt32, p->comm, s));
+    // D
+    if ((st = band_phase_d(b, x, self, n_components, s)) != CCL_OK) return st;
     // E
     return band_phase_e(b, x, band_labels, s, ev);
 }

@@ -79,8 +79,10 @@ struct Workspace {
     int32_t *k1hint_dev = nullptr;                  // device address of the word
     const volatile int32_t *k1hint_host = nullptr;  // host address (-1: nothing seen yet)
     // row bands only (null for a whole image):
-    const int32_t *xlab;  // [nb*2W]           exported labels of all bands' boundary slots; a
-                          //                   node whose parent is -2-f takes xlab[f]
+    const int32_t *xlab;  // [nb][2W+1]        gathered band records (N_band, then the band-local
+                          //                   labels of its boundary slots); a node whose parent
+                          //                   is -2-f (f = k*2W + s) takes record k's label s
+                          //                   plus the N of bands before k
     const int32_t *boff;  // [1]               labels of earlier bands (added to every label)
 };
 
@@ -161,10 +163,14 @@ cudaError_t band_resolve(int nb, int W, const int64_t *keys, const int32_t *reps
 // Link this band's components whose class starts in another component.
 cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys, const int32_t *spar,
                       const int32_t *nodes, cudaStream_t stream);
-// Global label of the root of each of n boundary slots (-1: not a root);
-// *boff = sum of counts of earlier bands; *n_total (if not null) = all.
+// Band-local label of the root of each of n boundary slots (-1: not a root),
+// into the band's record of the gathered table (record = N_band, then 2W
+// labels; labels_out = record + 1).
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
-                        int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
                         cudaStream_t stream);
+// After the gather of all nb records: *boff = N of earlier bands, *n_total
+// (if not null) = N of all bands.
+cudaError_t band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total,
+                         cudaStream_t stream);
 
 }  // namespace cclb

@@ -1071,7 +1071,12 @@ __device__ __forceinline__ void fixup_tile(const Geometry &g, const Workspace &w
     const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
     const uint64_t keep = pol_evict_last();  // the labels stay in L2 for K5
     auto root_label = [&](int r) -> int32_t {
-        if (r < 0) return __ldcg(ws.xlab + (-2 - r)) - *ws.boff;  // a root owned by another band
+        if (r < 0) {  // a root owned by another band: its band-local label + that band's offset
+            const int f = -2 - r, k = f / (2 * g.W), stride = 2 * g.W + 1;
+            int off = 0;
+            for (int j = 0; j < k; j++) off += __ldcg(ws.xlab + (size_t)j * stride);
+            return __ldcg(ws.xlab + (size_t)k * stride + 1 + (f - k * 2 * g.W)) + off - *ws.boff;
+        }
         return __ldcg(ws.gnodelab + r);
     };
     // the non-root's position among the tile's non-root border components
@@ -1932,28 +1937,32 @@ __global__ void k_xb_apply(int W, int self, const int64_t *keys, const int32_t *
     if (keys[r] == keys[t]) return;  // the class starts with this component
     gparent[nodes[s]] = r / (2 * W) == self ? nodes[r - self * 2 * W] : -2 - r;
 }
-// Global label of the root of every boundary slot of this band (-1: not a
-// root after the cross-band links); the band offset (labels of earlier
-// bands, from the gathered counts) is computed by every thread and stored
-// once for K4/K5, with the total N.
-__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int n, int nb, int self,
-                              const int32_t *counts, int32_t *boff, int32_t *n_total) {
+// Band-local label of the root of every boundary slot of this band (-1: not
+// a root after the cross-band links), written into the band's record of the
+// gathered table (N_band is its entry 0, K3's output): one all-gather then
+// carries both, and every rank adds the band offsets itself.
+__global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, int32_t *out, int n) {
     pdl_trigger();
     pdl_wait();
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int v = nodes[s];
+    out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) : -1;
+}
+// After the gather: this band's offset (labels of earlier bands) for K4/K5,
+// and the total N.  recs: nb records of 2W+1 ints, N_band first.
+__global__ void k_band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total) {
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x != 0) return;
     int off = 0, tot = 0;
     for (int k = 0; k < nb; k++) {
-        const int c = __ldcg(counts + k);
+        const int c = __ldcg(recs + (size_t)k * (2 * W + 1));
         off += k < self ? c : 0;
         tot += c;
     }
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s == 0) {
-        *boff = off;
-        if (n_total) *n_total = tot;
-    }
-    if (s >= n) return;
-    const int v = nodes[s];
-    out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) + off : -1;
+    *boff = off;
+    if (n_total) *n_total = tot;
 }
 
 // ==================================================================== host
@@ -2213,10 +2222,12 @@ cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys,
 }
 
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
-                        int nb, int self, const int32_t *counts, int32_t *boff, int32_t *n_total,
                         cudaStream_t stream) {
-    return launch_pdl(k_band_export, (n + 255) / 256, 256, 0, stream, g, ws, nodes, labels_out, n, nb, self, counts,
-                      boff, n_total);
+    return launch_pdl(k_band_export, (n + 255) / 256, 256, 0, stream, g, ws, nodes, labels_out, n);
+}
+cudaError_t band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total,
+                         cudaStream_t stream) {
+    return launch_pdl(k_band_offsets, 1, 32, 0, stream, recs, nb, W, self, boff, n_total);
 }
 
 }  // namespace cclb
