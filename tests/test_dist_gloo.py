@@ -1,9 +1,11 @@
 """The multi-GPU row-band protocol's host logic at world_size 2 on CPU (gloo):
 each rank labels its band with a plain reference, exchanges its boundary-row
 keys through torch.distributed (gloo), resolves the cross-band classes with
-the library's ccl_xband_resolve (pure host code, no GPU), numbers its roots
-after the earlier bands (all-gathered counts) and imports foreign labels --
-the same steps ccl_label_sharded runs over NCCL.  The gathered labels must
+the library's ccl_xband_resolve (pure host code, no GPU), numbers its roots,
+all-gathers one record per band (its root count and the band-local labels of
+its boundary-row roots), numbers after the earlier bands and imports foreign
+labels (band-local label + that band's offset) -- the same steps
+ccl_label_sharded runs over NCCL.  The gathered labels must
 equal the whole-image oracle bit for bit."""
 import os
 import socket
@@ -77,7 +79,9 @@ def _worker(rank, world, port, img, out_q):
     nlab = len(keys) - 1
     # a band label is a global root unless its class minimum is another key
     root = np.array([cmin.get(int(keys[l]), int(keys[l])) == int(keys[l]) for l in range(1, nlab + 1)], bool)
-    # C + X2: number global roots in raster order of their keys, after earlier bands
+    # C: number the band's global roots in raster order of their keys
+    # (band-local labels 1..rk), and the band-local labels of its own
+    # boundary-row roots: the band's record (rk, 2W labels)
     order = np.argsort(keys[1:])
     local = np.zeros(nlab + 1, np.int64)
     rk = 0
@@ -85,34 +89,36 @@ def _worker(rank, world, port, img, out_q):
         if root[j]:
             rk += 1
             local[j + 1] = rk
-    counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(counts, torch.tensor([rk], dtype=torch.int64))
-    off = int(sum(int(counts[k].item()) for k in range(rank)))
-    final = np.where(local > 0, local + off, 0)
-    # D + X3: export labels of own boundary-row roots, import foreign ones
     exp = np.full((2, W), -1, dtype=np.int64)
     key_to_label = {int(keys[l]): l for l in range(1, nlab + 1)}
     for r in range(2):
         for c in range(W):
             k = int(my_rows[r, c])
-            if k >= 0 and final[key_to_label[k]] > 0:
-                exp[r, c] = final[key_to_label[k]]
-    gexp = [torch.zeros((2, W), dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(gexp, torch.from_numpy(exp.astype(np.int64)))
+            if k >= 0 and local[key_to_label[k]] > 0:
+                exp[r, c] = local[key_to_label[k]]
+    rec = np.concatenate([[rk], exp.ravel()]).astype(np.int64)
+    # X2: one all-gather of the records (counts and foreign labels together)
+    recs = [torch.zeros(1 + 2 * W, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(recs, torch.from_numpy(rec))
+    counts = [int(recs[k][0].item()) for k in range(world)]
+    # D: this band's offset = N of the earlier bands
+    offs = [sum(counts[:k]) for k in range(world)]
+    final = np.where(local > 0, local + offs[rank], 0)
+    # a foreign root's label = its band-local label + its band's offset
     labmap = {}
     for k in range(world):
-        kk, ee = gathered[k].numpy(), gexp[k].numpy()
+        kk, ee = gathered[k].numpy(), recs[k][1:].numpy().reshape(2, W)
         for r in range(2):
             for c in range(W):
                 if ee[r, c] > 0:
-                    labmap[int(kk[r, c])] = int(ee[r, c])
+                    labmap[int(kk[r, c])] = int(ee[r, c]) + offs[k]
     # E: every band label -> its root's label (own or foreign)
     for l in range(1, nlab + 1):
         if not root[l - 1]:
             m = cmin[int(keys[l])]
             final[l] = labmap[m] if m in labmap else final[key_to_label[m]]
     out = final[lab].astype(np.int32)
-    total = int(sum(int(c.item()) for c in counts))
+    total = int(sum(counts))
     outs = [None] * world
     dist.all_gather_object(outs, (row0, out, total))
     if rank == 0:
@@ -121,9 +127,10 @@ def _worker(rank, world, port, img, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["c4_voronoi_21600", "c5a_serpentine_16384", "c3_percolation_8192",
-                                  "c5b_comb_16384"])
-def test_two_rank_band_protocol_matches_oracle(kind):
+@pytest.mark.parametrize("kind,world", [("c4_voronoi_21600", 2), ("c5a_serpentine_16384", 2),
+                                        ("c3_percolation_8192", 2), ("c5b_comb_16384", 2),
+                                        ("c5b_comb_16384", 3), ("c4_voronoi_21600", 3)])
+def test_two_rank_band_protocol_matches_oracle(kind, world):
     sys.path.insert(0, ROOT)
     import build_native
     build_native.build_product()
@@ -133,7 +140,7 @@ def test_two_rank_band_protocol_matches_oracle(kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, img, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, img, q)) for r in range(world)]
     for p in procs:
         p.start()
     outs = q.get(timeout=240)
