@@ -1673,7 +1673,10 @@ static bool small_mode(const Geometry &g) {
 // Labeling phase: one warp per 1024-px row segment.  Lane
 // j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
 // warp is one contiguous 512-byte stretch of the output row.
-constexpr int K5_WARPS = 16;  // measured vs 4 and 8
+#ifndef CCL_K5_WARPS
+#define CCL_K5_WARPS 8
+#endif
+constexpr int K5_WARPS = CCL_K5_WARPS;  // 8 CTAs/SM; measured vs 4 and 16 (C4 step -6 us vs 16 since the 256-bit stores)
 // (x & bit) ? v : 0
 __device__ __forceinline__ int sel_bit(uint32_t x, uint32_t bit, int v) {
     int r;
@@ -1681,7 +1684,7 @@ __device__ __forceinline__ int sel_bit(uint32_t x, uint32_t bit, int v) {
         : "=r"(r) : "r"(x & bit), "r"(v));
     return r;
 }
-__global__ void __launch_bounds__(K5_WARPS * 32, 4)
+__global__ void __launch_bounds__(K5_WARPS * 32, 64 / K5_WARPS)
 k_write(Geometry g, Workspace ws, int32_t *__restrict__ labels, uint32_t magic, int mshift) {
     pdl_trigger();
     pdl_wait();
