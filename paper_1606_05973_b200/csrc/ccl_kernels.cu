@@ -945,7 +945,10 @@ k_tile_big(const uint8_t *__restrict__ img, Geometry g, Workspace ws, int stop) 
 // runs of the last row above and the first row below are united along the
 // same two edge families as the strip merge.  Vertical tile edges (incl.
 // corner pixels): one thread per (tile column boundary, row).
-constexpr int K2_WARPS = 4;  // measured vs 2 and 8 warps per CTA
+#ifndef CCL_K2_WARPS
+#define CCL_K2_WARPS 4
+#endif
+constexpr int K2_WARPS = CCL_K2_WARPS;  // measured vs 2 and 8 warps per CTA
 __global__ void __launch_bounds__(K2_WARPS * 32)
 k_border(Geometry g, Workspace ws, int nh_warps, int hsplit) {
     pdl_trigger();
@@ -2080,7 +2083,10 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
     } else {
         auto k1 = g.thr ? (batch ? k_tile_local<true, true> : bands ? k_tile_local<true, false, true> : k_tile_local<true, false>)
                         : (batch ? k_tile_local<false, true> : bands ? k_tile_local<false, false, true> : k_tile_local<false, false>);
-        const int pfd = g_k1_exper ? 0 : g_k1_resident / 4;
+#ifndef CCL_PFD_DIV
+#define CCL_PFD_DIV 4
+#endif
+        const int pfd = g_k1_exper ? 0 : g_k1_resident / CCL_PFD_DIV;
         const bool twod = g.nTy <= 65535;
         e = launch_pdl2(k1, twod ? dim3(g.nTx, g.nTy) : dim3(g.nT), K1_THREADS, sizeof(K1SmemT<K1_MR>), stream, img, g,
                         ws, pfd, pfd % g.nTx, pfd / g.nTx, g_k1_stop);
