@@ -1168,7 +1168,7 @@ struct KNSmem {
 // NWN warps per tile-row CTA (8; fewer for images of 1-4 tile columns, so
 // the idle warps do not hold SM slots: C2 batches of 1024-px-wide images).
 template <int NWN>
-__global__ void __launch_bounds__(NWN * 32, NWN == 8 ? 6 : 16)
+__global__ void __launch_bounds__(NWN * 32, NWN >= 16 ? 64 / NWN : NWN == 8 ? 6 : 16)
 k_number(Geometry g, Workspace ws, int32_t *n_components) {
 #if CCL_K3_TRACE
     const unsigned long long t_in = gtimer();
@@ -2125,9 +2125,17 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
 cudaError_t run_stage_count(const Geometry &g, const Workspace &ws, int32_t *n_components,
                             cudaStream_t stream, cudaEvent_t *ev) {
     if (ev) cudaEventRecord(ev[0], stream);
-    const int nw = g.nTx >= 8 ? 8 : g.nTx >= 4 ? 4 : g.nTx >= 2 ? 2 : 1;
+    // warps per tile-row CTA: one per tile column up to 8; with few tile rows
+    // (row bands, mid-size images) 16 or 32, while every CTA of the grid is
+    // still resident at once (the lookback waits on earlier tile rows; with
+    // C4's 675 tile rows 16 warps did not fit and measured slower)
+    const int64_t warps_resident = (int64_t)g_sms * 64;
+    int nw = g.nTx >= 8 ? 8 : g.nTx >= 4 ? 4 : g.nTx >= 2 ? 2 : 1;
+    if (g.nTx > 16 && (int64_t)g.nTy * 32 <= warps_resident) nw = 32;
+    else if (g.nTx > 8 && (int64_t)g.nTy * 16 <= warps_resident) nw = 16;
     void (*k3)(Geometry, Workspace, int32_t *) =
-        nw == 8 ? k_number<8> : nw == 4 ? k_number<4> : nw == 2 ? k_number<2> : k_number<1>;
+        nw == 32 ? k_number<32> : nw == 16 ? k_number<16> : nw == 8 ? k_number<8> : nw == 4 ? k_number<4>
+        : nw == 2 ? k_number<2> : k_number<1>;
     cudaError_t e = launch_pdl(k3, g.nTy, nw * 32, 0, stream, g, ws, n_components);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
