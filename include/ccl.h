@@ -23,7 +23,9 @@
  * Sizes: 1 <= H, 1 <= W, (int64)H*W <= INT32_MAX.
  * Alignment: none required.  16-byte vector loads/stores are used only when
  * W % 16 == 0 AND the img (loads) / labels (stores) base pointer is 16-byte
- * aligned; otherwise the kernels fall back to narrower accesses.
+ * aligned, 32-byte ones only when the rows are 32-byte aligned as well (img:
+ * W % 32 == 0 and a 32-byte aligned base; labels: a 32-byte aligned base);
+ * otherwise the kernels fall back to narrower accesses.
  *
  * Ordering: the first kernel of a call waits for the previous work on
  * `stream` (e.g. the caller's kernel that produced img) to complete before it
