@@ -1864,12 +1864,32 @@ k_band_rows(Geometry g, Workspace ws, int64_t *keys, int32_t *nodes, unsigned lo
     const uint16_t *rc = ws.runcomp + ((int64_t)row * g.nTx + tx) * g.maxrun;
     const int32_t *compnode = ws.compnode + (int64_t)tile * g.capc;
     const int32_t *rowfirst = ws.meta + (int64_t)tile * META + META_ROWFIRST;
-    // root node and key once per run ...
-    for (int k = lane; k < (int)nr; k += 32) {
-        const uint32_t v = rc[k];  // (root row << 9) | rank
-        const int node = gfind_ro(ws.gparent, compnode[rowfirst[v >> 9] + (int)(v & 0x1FFu)]);
-        s_node[wi][k] = node;
-        s_key[wi][k] = ws.gkey[node];
+    // root node and key once per run, two runs per lane in flight together
+    // (the chain rc -> rowfirst -> compnode -> parents -> key is all latency)
+    for (int k = lane; k < (int)nr; k += 64) {
+        const int k2 = k + 32;
+        const bool two = k2 < (int)nr;
+        const uint32_t v = rc[k], v2 = two ? rc[k2] : 0u;  // (root row << 9) | rank
+        const int f = rowfirst[v >> 9], f2 = two ? rowfirst[v2 >> 9] : 0;
+        int x = compnode[f + (int)(v & 0x1FFu)], x2 = two ? compnode[f2 + (int)(v2 & 0x1FFu)] : -1;
+        // read-only finds in lockstep (a negative parent: a foreign root, terminal)
+        bool a1 = x >= 0, a2 = two && x2 >= 0;
+        while (a1 || a2) {
+            const int p1 = a1 ? __ldcg(ws.gparent + x) : 0, p2 = a2 ? __ldcg(ws.gparent + x2) : 0;
+            if (a1) {
+                if (p1 == x || p1 < 0) { a1 = false; x = p1 == x ? x : p1; } else x = p1;
+            }
+            if (a2) {
+                if (p2 == x2 || p2 < 0) { a2 = false; x2 = p2 == x2 ? x2 : p2; } else x2 = p2;
+            }
+        }
+        const int64_t key = ws.gkey[x], key2 = two ? ws.gkey[x2] : 0;
+        s_node[wi][k] = x;
+        s_key[wi][k] = key;
+        if (two) {
+            s_node[wi][k2] = x2;
+            s_key[wi][k2] = key2;
+        }
     }
     __syncwarp();
     // ... then per pixel, lane = pixel within each 32-pixel word (coalesced)
