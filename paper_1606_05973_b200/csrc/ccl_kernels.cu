@@ -2,7 +2,7 @@
 // pipeline.  DESIGN.md explains the design; paper citations are PAPER.md lines.
 //
 //   K1 k_tile_local   one CTA per 32x1024 image tile: reads the pixels once
-//                     (16-byte streaming loads; fg = byte != 0),
+//                     (32-byte streaming loads; fg = byte != 0),
 //                     packs them to row masks and fills bridged single-pixel
 //                     holes; the runs of the tile are its provisional labels
 //                     (index order = raster order).  Scan: every run copies its
@@ -23,7 +23,7 @@
 //   K4 k_fixup        labels of the border components that are not global roots
 //                     (their root's label).
 //   K5 k_write        labeling phase: every pixel gets its
-//                     component's label; coalesced 16-byte streaming stores.
+//                     component's label; coalesced 32-byte stores (evict_first).
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <stdint.h>
@@ -1674,8 +1674,9 @@ static bool small_mode(const Geometry &g) {
 
 // ========================================================================= K5
 // Labeling phase: one warp per 1024-px row segment.  Lane
-// j writes pixels 128c + 4j .. +3 (c = 0..7), so every 16-byte store of the
-// warp is one contiguous 512-byte stretch of the output row.
+// j writes pixels 256c + 8j .. +7 (c = 0..3), so every 32-byte store of the
+// warp is one contiguous 1 KB stretch of the output row (rows not 32-byte
+// aligned: pixels 128c + 4j .. +3 with 16-byte stores).
 #ifndef CCL_K5_WARPS
 #define CCL_K5_WARPS 8
 #endif
