@@ -261,9 +261,12 @@ __device__ __forceinline__ int gfind_halve(int32_t *par, int x) {
 __device__ void gunion(int32_t *par, const int64_t *key, int a, int b) {
     while (true) {
         a = gfind(par, a);
+        // a's key is in flight during the second find (C5a serpentine K2
+        // 109 -> 73 us; C4 unchanged)
+        const int64_t ka = __ldg(key + a);
         b = gfind(par, b);
         if (a == b) return;
-        if (__ldg(key + a) < __ldg(key + b)) { int t = a; a = b; b = t; }
+        if (ka < __ldg(key + b)) { int t = a; a = b; b = t; }
         if (atomicCAS(par + a, a, b) == a) return;
     }
 }
