@@ -2122,9 +2122,11 @@ cudaError_t run_stage_local(const Geometry &g0, const Workspace &ws, const uint8
         // a small grid (usually there is nothing to do; its CTAs loop over the list)
         // (a plan's last known hand-over count of 0: a quarter of the SMs, so
         // that every CTA fits beside K1's last wave and K2 is scheduled at
-        // once -- C4 step 661 -> 650 us; otherwise half the resident slots)
+        // once -- C4 step 661 -> 650 us; otherwise every resident slot: the
+        // comb hands every tile over, K1 1.50 -> 0.82 ms against half the
+        // slots)
         const bool idle = ws.k1hint_host && *ws.k1hint_host == 0;
-        const int grid = idle ? std::max(1, g_sms / 4) : g_k1big_resident / 2;
+        const int grid = idle ? std::max(1, g_sms / 4) : g_k1big_resident;
         e = launch_pdl(k1b, std::min(g.nT, grid), NW * 32, sizeof(K1Smem), stream, img, g, ws, g_k1_stop);
         if (e != cudaSuccess) return e;
     }
