@@ -413,9 +413,9 @@ def main():
         plan = None
         # our kernels per band step (ccl_bands.cu): K1 (+ its hand-over pass), K2, boundary rows
         # (+ representative minima), slot representatives (+ the slot union-find's start),
-        # slot unions, link, K3, export, band offset, K4, K5 (the 2 NCCL
+        # slot unions, link, K3, export, K4 (+ band offset), K5 (the 2 NCCL
         # all-gathers are not counted)
-        launches_per_step = 12
+        launches_per_step = 11
 
     for _ in range(max(3, args.warmup)):
         step()

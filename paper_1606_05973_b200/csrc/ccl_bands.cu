@@ -25,7 +25,8 @@
 //      foreign-label table and the counts in one collective (a foreign
 //      root's label = its band-local label + the N of the bands before its
 //      band; round 1 gathered N and the labels in two)
-//   D  offset of this band = sum of N over earlier bands; N
+//   D  offset of this band = sum of N over earlier bands; N (K4's first
+//      thread, from the gathered records)
 //   E  labels of merged components + label write
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -215,15 +216,15 @@ ccl_status band_phase_bc(Band &b, const XBand &x, int self, cudaStream_t s, cuda
     return CCL_OK;
 }
 
-// D (every record gathered): the band offset (N of earlier bands) and N
-ccl_status band_phase_d(Band &b, const XBand &x, int self, int32_t *n_total, cudaStream_t s) {
-    CK(band_offsets(x.recs, x.nb, x.W, self, b.d_small + 1, n_total, s));
-    return CCL_OK;
-}
-
-// E: labels of merged components (foreign ones from the gathered records) + write
-ccl_status band_phase_e(Band &b, const XBand &x, int32_t *labels, cudaStream_t s, cudaEvent_t *ev = nullptr) {
+// D + E (every record gathered): labels of merged components (foreign ones
+// from the gathered records; K4's first thread also stores the band offset =
+// N of the earlier bands, and N) + label write
+ccl_status band_phase_e(Band &b, const XBand &x, int self, int32_t *n_total, int32_t *labels, cudaStream_t s,
+                        cudaEvent_t *ev = nullptr) {
     b.ws.xlab = x.recs;
+    b.ws.xself = self;
+    b.ws.xnb = x.nb;
+    b.ws.xntotal = n_total;
     CK(run_stage_final(b.g, b.ws, labels, s, ev ? ev + 5 : nullptr));  // ev[5], ev[6], ev[7]
     return CCL_OK;
 }
@@ -272,12 +273,11 @@ ccl_status ccl_label_banded(const uint8_t *img, int H, int W, int nbands, int32_
     // B + C (+ X2: every band writes its record straight into the shared table)
     for (int k = 0; k < nbands; k++)
         if ((st = band_phase_bc(bands[k], x, k, s)) != CCL_OK) return st;
-    // D
+    // D + E
     for (int k = 0; k < nbands; k++)
-        if ((st = band_phase_d(bands[k], x, k, k == 0 ? n_components : nullptr, s)) != CCL_OK) return st;
-    // E
-    for (int k = 0; k < nbands; k++)
-        if ((st = band_phase_e(bands[k], x, labels + (size_t)r0[k] * W, s)) != CCL_OK) return st;
+        if ((st = band_phase_e(bands[k], x, k, k == 0 ? n_components : nullptr, labels + (size_t)r0[k] * W, s)) !=
+            CCL_OK)
+            return st;
     CK(cudaStreamSynchronize(s));  // the band workspaces are freed on return
     return CCL_OK;
 }
@@ -402,10 +402,8 @@ ccl_status ccl_shard_plan_label(ccl_shard_plan p, const uint8_t *band_img, int32
     // X2: every band's record (N_band + its slots' band-local root labels)
     const size_t rec = slots + 1;
     CKN(ncclAllGather(x.recs + self * rec, x.recs, rec, ncclInt32, p->comm, s));
-    // D
-    if ((st = band_phase_d(b, x, self, n_components, s)) != CCL_OK) return st;
-    // E
-    return band_phase_e(b, x, band_labels, s, ev);
+    // D + E
+    return band_phase_e(b, x, self, n_components, band_labels, s, ev);
 }
 
 ccl_status ccl_shard_plan_set_profiling(ccl_shard_plan p, int nsets) {

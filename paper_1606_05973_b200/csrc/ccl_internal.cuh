@@ -83,7 +83,10 @@ struct Workspace {
                           //                   labels of its boundary slots); a node whose parent
                           //                   is -2-f (f = k*2W + s) takes record k's label s
                           //                   plus the N of bands before k
-    const int32_t *boff;  // [1]               labels of earlier bands (added to every label)
+    const int32_t *boff;  // [1]               labels of earlier bands (added to every label by K5;
+                          //                   written by K4's first thread from the records)
+    int xself = 0, xnb = 0;         // this band's index, the number of bands
+    int32_t *xntotal = nullptr;     // [1] N of all bands (K4 writes it; null: not wanted)
 };
 
 Geometry make_geometry(int H, int W);
@@ -168,9 +171,6 @@ cudaError_t band_link(const Workspace &ws, int W, int self, const int64_t *keys,
 // labels; labels_out = record + 1).
 cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *nodes, int32_t *labels_out, int n,
                         cudaStream_t stream);
-// After the gather of all nb records: *boff = N of earlier bands, *n_total
-// (if not null) = N of all bands.
-cudaError_t band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total,
-                         cudaStream_t stream);
+
 
 }  // namespace cclb

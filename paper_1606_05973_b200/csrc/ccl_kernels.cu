@@ -1077,11 +1077,15 @@ __device__ __forceinline__ void fixup_tile(const Geometry &g, const Workspace &w
     const int32_t *twpre = ws.twpre + (int64_t)tile * g.capw;
     const uint64_t keep = pol_evict_last();  // the labels stay in L2 for K5
     auto root_label = [&](int r) -> int32_t {
-        if (r < 0) {  // a root owned by another band: its band-local label + that band's offset
+        if (r < 0) {  // a root owned by another band: its band-local label + that band's
+                      // offset, less this band's (the label stored here is band-local)
             const int f = -2 - r, k = f / (2 * g.W), stride = 2 * g.W + 1;
             int off = 0;
-            for (int j = 0; j < k; j++) off += __ldcg(ws.xlab + (size_t)j * stride);
-            return __ldcg(ws.xlab + (size_t)k * stride + 1 + (f - k * 2 * g.W)) + off - *ws.boff;
+            for (int j = 0; j < max(k, ws.xself); j++) {
+                const int c = __ldcg(ws.xlab + (size_t)j * stride);
+                off += (j < k ? c : 0) - (j < ws.xself ? c : 0);
+            }
+            return __ldcg(ws.xlab + (size_t)k * stride + 1 + (f - k * 2 * g.W)) + off;
         }
         return __ldcg(ws.gnodelab + r);
     };
@@ -1120,6 +1124,18 @@ __global__ void __launch_bounds__(K4_WARPS * 32)
 k_fixup(Geometry g, Workspace ws) {
     pdl_trigger();
     pdl_wait();
+    if (ws.xlab && blockIdx.x == 0 && threadIdx.x == 0) {
+        // row bands: this band's offset (N of the earlier bands, for K5) and
+        // N from the gathered records (N_band first in each)
+        int off = 0, tot = 0;
+        for (int k = 0; k < ws.xnb; k++) {
+            const int c = __ldcg(ws.xlab + (size_t)k * (2 * g.W + 1));
+            off += k < ws.xself ? c : 0;
+            tot += c;
+        }
+        *const_cast<int32_t *>(ws.boff) = off;
+        if (ws.xntotal) *ws.xntotal = tot;
+    }
     const int tile = blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     if (tile >= g.nT) return;
     fixup_tile(g, ws, tile, lane_id());
@@ -1979,21 +1995,6 @@ __global__ void k_band_export(Geometry g, Workspace ws, const int32_t *nodes, in
     const int v = nodes[s];
     out[s] = (v >= 0 && __ldcg(ws.gparent + v) == v) ? __ldcg(ws.gnodelab + v) : -1;
 }
-// After the gather: this band's offset (labels of earlier bands) for K4/K5,
-// and the total N.  recs: nb records of 2W+1 ints, N_band first.
-__global__ void k_band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total) {
-    pdl_trigger();
-    pdl_wait();
-    if (threadIdx.x != 0) return;
-    int off = 0, tot = 0;
-    for (int k = 0; k < nb; k++) {
-        const int c = __ldcg(recs + (size_t)k * (2 * W + 1));
-        off += k < self ? c : 0;
-        tot += c;
-    }
-    *boff = off;
-    if (n_total) *n_total = tot;
-}
 
 // ==================================================================== host
 static bool g_attr_done = false;
@@ -2268,9 +2269,6 @@ cudaError_t band_export(const Geometry &g, const Workspace &ws, const int32_t *n
                         cudaStream_t stream) {
     return launch_pdl(k_band_export, (n + 255) / 256, 256, 0, stream, g, ws, nodes, labels_out, n);
 }
-cudaError_t band_offsets(const int32_t *recs, int nb, int W, int self, int32_t *boff, int32_t *n_total,
-                         cudaStream_t stream) {
-    return launch_pdl(k_band_offsets, 1, 32, 0, stream, recs, nb, W, self, boff, n_total);
-}
+
 
 }  // namespace cclb
