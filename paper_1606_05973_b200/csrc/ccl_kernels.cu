@@ -752,10 +752,12 @@ __device__ __forceinline__ void k1_tile(const uint8_t *__restrict__ img, const G
                 uint32_t r = j;
                 // (j is never flagged: only this warp ranks its own runs,
                 // below; j == k: a root, no second load)
+                // (a non-root's parent is below it; a root points to itself or
+                // holds 0x8000 | rank > any index: one compare stops at both)
                 if (j != (uint32_t)k)
                     while (true) {
                         const uint32_t v = vp[r];
-                        if (v == r || (v & 0x8000u)) break;
+                        if (v >= r) break;
                         r = v;
                     }
                 root = r == (uint32_t)k;
