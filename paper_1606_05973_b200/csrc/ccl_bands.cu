@@ -106,10 +106,13 @@ struct Band {
     size_t noderep_count = 0;
     uint32_t epoch = 0;              // calls on this band (band_rep's epoch)
     int32_t *d_small = nullptr;    // [0] N_band, [1] band offset
+    int32_t *hint = nullptr;       // mapped pinned host word: K1's last hand-over count (Workspace::k1hint_dev)
     int band_H = 0, row0 = 0;
 
     ~Band() { release(); }
     void release() {
+        if (hint) cudaFreeHost(hint);
+        hint = nullptr;
         if (mem) cudaFree(mem);
         if (d_nodes) cudaFree(d_nodes);
         if (d_noderep) cudaFree(d_noderep);
@@ -170,6 +173,17 @@ ccl_status band_init(Band &b, int band_H, int W, int row0) {
     CK(cudaMemset(b.d_noderep, 0xFF, sizeof(unsigned long long) * b.noderep_count));
     CK(cudaMalloc(&b.d_small, sizeof(int32_t) * 4));
     b.ws.boff = b.d_small + 1;
+    // the hand-over hint (as a plan's): later band steps launch K1's idle
+    // hand-over pass small
+    int32_t *hint_dev = nullptr;
+    if (cudaHostAlloc(&b.hint, sizeof(int32_t), cudaHostAllocMapped) == cudaSuccess) {
+        *b.hint = -1;
+        if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&hint_dev), b.hint, 0) == cudaSuccess) {
+            b.ws.k1hint_dev = hint_dev;
+            b.ws.k1hint_host = b.hint;
+        }
+    }
+    cudaGetLastError();  // (no hint: the full hand-over grid every step)
     return CCL_OK;
 }
 
