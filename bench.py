@@ -339,26 +339,41 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    import numpy as np
     import synth
     img = synth.generate(args.workload)
     H, W = img.shape
     import oracle
-    for _ in range(args.warmup):
-        oracle.label(img)
+    # each step labels a bounded sample: the whole image while the run fits in
+    # about two minutes, else the first rows of it (a row band, as PARemSP's
+    # chunks) sized to that budget -- the rate is per pixel either way
+    t0 = time.perf_counter()
+    oracle.label(img)
+    t_full = time.perf_counter() - t0
+    budget_s = 120.0
+    rows = H
+    if (args.steps + max(0, args.warmup - 1)) * t_full > budget_s:
+        rows = max(1, int(H * budget_s / ((args.steps + max(0, args.warmup - 1)) * t_full)))
+    sample = np.ascontiguousarray(img[:rows]) if rows < H else img
+    for _ in range(max(0, args.warmup - 1)):
+        oracle.label(sample)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.label(img)
+        oracle.label(sample)
         ts.append(time.perf_counter() - t0)
     t = sum(ts) / len(ts)
-    v = H * W / t / 1e9
+    v = rows * W / t / 1e9
+    t = H * W / (v * 1e9)  # per full image at the measured rate
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gpx/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic", "config": {"workload": args.workload, "H": H, "W": W},
         "cpu_baseline": {"value": v, "unit": "Gpx/s", "cores": 1, "kind": "oracle",
-                         "sample": f"full {H}x{W} {args.workload} image per step (single-threaded C oracle)"},
+                         "sample": (f"full {H}x{W} {args.workload} image per step" if rows == H else
+                                    f"first {rows} of {H} rows of the {H}x{W} {args.workload} image per step "
+                                    f"(the run bounded to ~{budget_s:.0f} s)") + " (single-threaded C oracle)"},
         "e2e": {"value": v, "unit": "Gpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     return 0
