@@ -117,7 +117,10 @@ ccl_status ccl_label_batch(const uint8_t *imgs, int B, int H, int W, int32_t *la
  * ---------------------------------------------------------------------- */
 typedef struct ccl_plan_st *ccl_plan;
 
-/* Allocates device workspace for H x W images on the current device. */
+/* Allocates device workspace for H x W images on the current device (and
+ * one mapped pinned host word: the plan sizes each call's hand-over pass for
+ * tiles with rows of > 256 runs from the count its earlier calls left there;
+ * outputs never depend on it). */
 ccl_status ccl_plan_create(int H, int W, ccl_plan *plan_out);
 /* Workspace for batches of B images of H x W (ccl_label_batch's layout): the
  * plan's label calls then take B*H*W pixels and write B component counts. */
