@@ -1016,9 +1016,23 @@ k_border(Geometry g, Workspace ws, int nh_warps, int hsplit) {
             }
             __syncwarp();
             const int np = min(PCAP, (int)tot - w0);
-            for (int i = 32 * hs + lane; i < np; i += 32 * hsplit) {
-                const uint32_t e = plist[wib][i];
-                gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
+            if (hsplit == 1) {
+                // consecutive entries often join the same two nodes (one region
+                // crossing the edge in several runs): a union equal to the
+                // previous lane's is skipped, as on the vertical edges (C4
+                // step -2 us; K4 then walks a little more)
+                for (int i0 = 0; i0 < np; i0 += 32) {
+                    const int i = i0 + lane;
+                    const uint32_t e = i < np ? plist[wib][i] : 0u;
+                    const int a = i < np ? bot[e & 0xFFFFu] : -1, b = i < np ? top[e >> 16] : -1;
+                    const int ap = __shfl_up_sync(FULL, a, 1), bp = __shfl_up_sync(FULL, b, 1);
+                    if (i < np && !(lane > 0 && ap == a && bp == b)) gunion(ws.gparent, ws.gkey, a, b);
+                }
+            } else {
+                for (int i = 32 * hs + lane; i < np; i += 32 * hsplit) {
+                    const uint32_t e = plist[wib][i];
+                    gunion(ws.gparent, ws.gkey, bot[e & 0xFFFFu], top[e >> 16]);
+                }
             }
             __syncwarp();
         }
