@@ -333,6 +333,42 @@ def dist_env():
     return ws, rank, local
 
 
+def two_streams(plan, d_img, H, W, dev, K):
+    """K frames of the workload alternating over two plans on two streams."""
+    import torch
+    import paper_1606_05973_b200 as ccl
+    plans = [plan, ccl.Plan(H, W, device=dev)]
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs = [torch.empty((H, W), dtype=torch.int32, device=dev) for _ in range(2)]
+    ns = [torch.empty(1, dtype=torch.int32, device=dev) for _ in range(2)]
+    cur = torch.cuda.current_stream(dev)
+
+    def run(k):
+        for i in range(k):
+            j = i & 1
+            plans[j].label(d_img, outs[j], ns[j], stream=streams[j])
+
+    for s in streams:
+        s.wait_stream(cur)
+    run(6)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(cur)
+    for s in streams:
+        s.wait_event(e0)
+    run(K)
+    for s in streams:
+        cur.wait_stream(s)
+    e1.record(cur)
+    torch.cuda.synchronize(dev)
+    us = e0.elapsed_time(e1) * 1e3 / K
+    same = bool(torch.equal(outs[0], outs[1]) and int(ns[0].item()) == int(ns[1].item()))
+    del plans[1]
+    return {"us_per_frame": us, "gpx_s": H * W / (us * 1e-6) / 1e9, "frames": K,
+            "labels_identical_across_plans": same,
+            "note": "two plans on two streams, frames alternating (serving context, not value)"}
+
+
 def run_reference(args):
     """The reference arm for this tier: the CPU oracle as it stands (plain C
     ARemSP + canonical renumbering, single-threaded) on the same workload."""
@@ -501,6 +537,13 @@ def main():
         "single_call_latency_ms": latency_ms,
         "roofline": roofline,
     }
+
+    # ---- serving context (not `value`): two frames in flight, two plans on
+    # two streams, frames alternating; device-resident, CUDA events.  Only the
+    # kernels' tails overlap (K5 takes every warp slot while it runs), see
+    # DESIGN.md section 11.
+    if ws == 1 and plan is not None and not args.no_small:
+        line["frames_two_streams"] = two_streams(plan, d_img, H, W, dev, args.steps)
 
     # ---- the paper's <= 1 MB regime (C1, C2): one image per call vs a batch
     # of 64 per call (ccl_label_batch), device-resident, CUDA events
