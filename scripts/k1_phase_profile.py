@@ -45,7 +45,7 @@ for l in dis.splitlines():
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/', l)
     if m:
         off2ph[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "-k", "regex:k_tile_local", "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "Address"][0]
@@ -53,10 +53,14 @@ hdr = rows[hi]
 iA, iI, iS = 0, hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 base = None
 agg = {}
+seen = set()
 for r in rows[hi + 1:]:
     if len(r) <= iI or not r[0].startswith("0x"):
         continue
     a = int(r[0], 16)
+    if a in seen:  # newer ncu lists the SASS page twice
+        continue
+    seen.add(a)
     base = a if base is None else base
     ph = off2ph.get(a - base, "?")
     n = int(r[iI] or 0); s = int(r[iS] or 0)
